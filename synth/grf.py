@@ -1,0 +1,178 @@
+"""Gaussian-random-field coefficient sampling (input synthesis only).
+
+Recipe; the paper only says the coefficient
+fields are "derived using GRF":
+
+    g(x) = sum_{k in {1..K}^d} xi_k (1 + |k|^2)^(-s) prod_d sin(k_d pi x_d),
+    xi_k ~ N(0, 1) from numpy default_rng(SeedSequence([23215, cfg, i, f])),
+    drawn in C order with shape (K,)*d indexed [k_x, k_y(, k_z)].
+
+Where the config gives sigma, g <- sigma * g / s_K with s_K the analytic
+domain-RMS standard deviation of the raw series (`grf_std`).  The coefficient
+is vscale * exp(g).  Unit square/cube, Dirichlet, h = 1/(nx+1); node i sits at
+x = (i+1) h and the face between node i-1 and node i at x = (i+1/2) h,
+i = 0..nx (i = 0 and i = nx are the boundary faces).
+
+Outputs per operator: the face coefficients a on every axis, the nodal
+reaction c (zero for -div(a grad u)) and the nodal parameter fields P used by
+the sort ("parameter matrices P"; P:1106 p = grid side).
+No FD assembly happens here: both the CUDA path and the oracle assemble A
+from these arrays with their own code.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+import numpy as np
+
+from .configs import Config, CONFIGS
+
+_CFG_INDEX = {name: i for i, name in enumerate(CONFIGS)}
+
+
+def grf_std(K: int, s: float, dim: int) -> float:
+    """Analytic domain-RMS std of the raw series: sqrt(sum_k w_k^2 (1/2)^d)."""
+    k = np.arange(1, K + 1, dtype=np.float64)
+    kk = np.zeros((K,) * dim)
+    for ax in range(dim):
+        shape = [1] * dim
+        shape[ax] = K
+        kk = kk + (k ** 2).reshape(shape)
+    return float(np.sqrt(((1.0 + kk) ** (-2.0 * s)).sum() * 0.5 ** dim))
+
+
+def _weights(K: int, s: float, dim: int) -> np.ndarray:
+    k = np.arange(1, K + 1, dtype=np.float64)
+    kk = np.zeros((K,) * dim)
+    for ax in range(dim):
+        shape = [1] * dim
+        shape[ax] = K
+        kk = kk + (k ** 2).reshape(shape)
+    return (1.0 + kk) ** (-s)
+
+
+def _sin_basis(coords: np.ndarray, K: int) -> np.ndarray:
+    k = np.arange(1, K + 1, dtype=np.float64)
+    return np.sin(np.pi * np.outer(coords, k))          # [len(coords), K]
+
+
+def _eval(coef: np.ndarray, bases: list[np.ndarray]) -> np.ndarray:
+    """g on the tensor grid given per-axis sine bases [x, y(, z)]; C order (z,) y, x."""
+    if len(bases) == 2:
+        bx, by = bases
+        return by @ coef.T @ bx.T                        # coef[kx, ky] -> g[y, x]
+    bx, by, bz = bases
+    return np.einsum("xa,yb,zc,abc->zyx", bx, by, bz, coef, optimize=True)
+
+
+@dataclass
+class OperatorFields:
+    """Coefficient arrays for a batch of N operators on one grid (float64, C order).
+
+    faces[ax] holds a at the face midpoints normal to axis ax:
+      2-D: faces[0] [N, ny, nx+1], faces[1] [N, ny+1, nx]
+      3-D: faces[0] [N, nz, ny, nx+1], faces[1] [N, nz, ny+1, nx], faces[2] [N, nz+1, ny, nx]
+    c: nodal reaction [N, n] (x fastest).  params: sort fields [N, F, n] (x fastest).
+    """
+    dim: int
+    nx: int
+    h: float
+    faces: list
+    c: np.ndarray
+    params: np.ndarray
+
+    @property
+    def n_ops(self) -> int:
+        return self.c.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.nx ** self.dim
+
+    def subset(self, idx) -> "OperatorFields":
+        idx = np.asarray(idx)
+        return OperatorFields(self.dim, self.nx, self.h,
+                              [np.ascontiguousarray(f[idx]) for f in self.faces],
+                              np.ascontiguousarray(self.c[idx]),
+                              np.ascontiguousarray(self.params[idx]))
+
+
+def _xi(cfg_index: int, i: int, f: int, K: int, dim: int) -> np.ndarray:
+    rng = np.random.default_rng(np.random.SeedSequence([23215, cfg_index, i, f]))
+    return rng.standard_normal((K,) * dim)
+
+
+def make_fields(cfg: Config, i: int, f: int, cfg_index: int | None = None):
+    """One GRF sample (operator i, field f) -> (nodal g, [face g per axis])."""
+    ci = _CFG_INDEX.get(cfg.name, 0) if cfg_index is None else cfg_index
+    dim, nx, K = cfg.dim, cfg.nx, cfg.K
+    h = cfg.h
+    coef = _xi(ci, i, f, K, dim) * _weights(K, cfg.s, dim)
+    if cfg.sigma is not None:
+        coef = coef * (cfg.sigma / grf_std(K, cfg.s, dim))
+    nodes = (np.arange(nx) + 1.0) * h
+    faces = (np.arange(nx + 1) + 0.5) * h
+    bn = _sin_basis(nodes, K)
+    bf = _sin_basis(faces, K)
+    g_node = _eval(coef, [bn] * dim)
+    g_face = []
+    for ax in range(dim):
+        bases = [bn] * dim
+        bases[ax] = bf
+        g_face.append(_eval(coef, bases))
+    return g_node, g_face
+
+
+def make_batch(cfg: Config, n_ops: int | None = None, start: int = 0) -> OperatorFields:
+    """Operators start..start+n_ops-1 of config `cfg` (seeded, deterministic)."""
+    N = cfg.n_ops if n_ops is None else n_ops
+    dim, nx = cfg.dim, cfg.nx
+    n = nx ** dim
+    shape_node = (nx,) * dim
+    face_shapes = []
+    for ax in range(dim):
+        s = [nx] * dim
+        s[dim - 1 - ax] = nx + 1                        # C order: axis x is last
+        face_shapes.append(tuple(s))
+    faces = [np.empty((N,) + fs) for fs in face_shapes]
+    c = np.zeros((N, n))
+    params = np.empty((N, cfg.fields, n))
+    for j in range(N):
+        i = start + j
+        if cfg.family == "lapv":
+            g_node, _ = make_fields(cfg, i, 0)
+            v = cfg.vscale * np.exp(g_node)
+            for ax in range(dim):
+                faces[ax][j] = 1.0
+            c[j] = v.reshape(n)
+            params[j, 0] = v.reshape(n)
+        elif cfg.family == "diva":
+            g_node, g_face = make_fields(cfg, i, 0)
+            for ax in range(dim):
+                faces[ax][j] = cfg.vscale * np.exp(g_face[ax])
+            params[j, 0] = (cfg.vscale * np.exp(g_node)).reshape(n)
+        elif cfg.family == "divac":
+            ga_node, ga_face = make_fields(cfg, i, 0)
+            gc_node, _ = make_fields(cfg, i, 1)
+            for ax in range(dim):
+                faces[ax][j] = np.exp(ga_face[ax])
+            c[j] = np.exp(gc_node).reshape(n)
+            params[j, 0] = np.exp(ga_node).reshape(n)
+            params[j, 1] = c[j]
+        else:
+            raise ValueError(cfg.family)
+    assert all(f.shape[1:] == fs for f, fs in zip(faces, face_shapes))
+    del shape_node
+    return OperatorFields(dim, nx, cfg.h, faces, c, params)
+
+
+def constant_fields(dim: int, nx: int, n_ops: int = 1, a: float = 1.0, c: float = 0.0) -> OperatorFields:
+    """Constant-coefficient batch (closed-form Laplacian spectrum cases)."""
+    n = nx ** dim
+    faces = []
+    for ax in range(dim):
+        s = [nx] * dim
+        s[dim - 1 - ax] = nx + 1
+        faces.append(np.full((n_ops,) + tuple(s), float(a)))
+    cc = np.full((n_ops, n), float(c))
+    params = np.full((n_ops, 1, n), float(a))
+    return OperatorFields(dim, nx, 1.0 / (nx + 1), faces, cc, params)
