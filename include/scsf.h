@@ -1,0 +1,203 @@
+/*
+ * scsf.h — C ABI of libscsf.so, the sm_100a hot path of SCSF
+ * (Sorting Chebyshev Subspace Filter, arXiv 2510.23215).
+ *
+ * Citations "P:n" are lines of the paper text /root/reference/PAPER.md
+ * (section / algorithm named alongside); DESIGN.md lists every reading taken
+ * where the paper is silent (R1..R24).
+ *
+ * Conventions shared by every entry point
+ *  - Plain C types only.  `stream` is a cudaStream_t passed as void* (NULL =
+ *    legacy default stream).  Every call is synchronous on return: it
+ *    enqueues its kernels on `stream` and synchronises that stream.
+ *  - Device pointers ("dev") are caller-owned (the Python side allocates them
+ *    with torch); host pointers ("host") are plain CPU memory.  The library
+ *    never allocates or frees device memory; scratch space comes from the
+ *    caller's `ws` (device, 256-byte aligned, at least the size reported by
+ *    the matching *_workspace_bytes query).
+ *  - Vector blocks are fp64, column-major: column j of an n-row block starts
+ *    at ptr + j*ld, with ld >= n.  Unknowns are ordered x fastest:
+ *    k = ix + nx*(iy + ny*iz)  (row-major grid order, Eq. 2).
+ *  - Return value: scsf_status.  On failure scsf_last_error() returns a
+ *    thread-local message.  No exception or abort crosses the ABI.
+ *  - Not re-entrant on one stream; distinct streams/devices are independent.
+ */
+#ifndef SCSF_H_
+#define SCSF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCSF_ABI_VERSION 1
+
+typedef enum {
+  SCSF_OK = 0,
+  SCSF_ERR_ARG = 1,             /* invalid argument (shape, range, NULL)            */
+  SCSF_ERR_NUMERICAL = 2,       /* not converged in max_iter / QR breakdown          */
+  SCSF_ERR_DEVICE = 3,          /* CUDA error (launch, memcpy, sync)                 */
+  SCSF_ERR_NOT_IMPLEMENTED = 4, /* configuration not supported by this build         */
+  SCSF_ERR_WORKSPACE = 5        /* ws NULL or ws_bytes below the queried size        */
+} scsf_status;
+
+/*
+ * A batch of discretised operators A^(i), i = 0..n_ops-1 (Eq. 3),
+ * each a real symmetric 5-point (dim 2) or 7-point (dim 3) stencil, stored
+ * as symmetric DIA arrays in device memory:
+ *   coef[(i*(1+dim) + 0)*ld + k] = A(k, k)           (diag)
+ *   coef[(i*(1+dim) + 1)*ld + k] = A(k, k+1)         (cx; 0 when ix = nx-1)
+ *   coef[(i*(1+dim) + 2)*ld + k] = A(k, k+nx)        (cy; 0 when iy = ny-1)
+ *   coef[(i*(1+dim) + 3)*ld + k] = A(k, k+nx*ny)     (cz; dim 3; 0 when iz = nz-1)
+ * ld >= n = nx*ny*nz, multiple of 32.  Produced by scsf_assemble() or by the
+ * caller.  The matrix must be symmetric positive definite for the solve
+ * (R20: flux form); eigenvalues are returned ascending, which is
+ * the |lambda| order of P:150 for SPD operators.
+ */
+typedef struct {
+  int32_t dim;          /* 2 or 3                                        */
+  int32_t nx, ny, nz;   /* interior grid size (nz = 1 when dim == 2)     */
+  int32_t n_ops;        /* operators in the batch                        */
+  int32_t reserved;     /* must be 0                                     */
+  int64_t ld;           /* stride between coefficient arrays (doubles)   */
+  const double* coef;   /* dev [n_ops][1+dim][ld]                        */
+} scsf_ops;
+
+/* Per-operator statistics (SPEC S:384-388 SolveRecord fields; P:463-479 Tab. sort1). */
+typedef struct {
+  int32_t status;            /* scsf_status of this operator                          */
+  int32_t iterations;        /* outer ChFSI iterations (Alg. 3 repeat loop)    */
+  int32_t filter_steps;      /* Chebyshev three-term steps applied (sum over iters)   */
+  int32_t cholqr_fallbacks;  /* shifted-CholQR fallbacks taken                        */
+  int32_t n_locked;          /* converged pairs locked at exit (>= L on success)      */
+  int32_t warm;              /* 1 if started from the previous operator's block       */
+  int64_t spmm_columns;      /* stencil applications x columns (filter + RR)          */
+  double max_rel_resid;      /* max over returned pairs of ||Av - lv|| / ||Av|| */
+  double beta;               /* spectral upper bound used by the filter (Gershgorin)  */
+  /* phase timers, CUDA events on the launching stream (0 unless scsf_set_timing(1)) */
+  double t_filter_ms;        /* Chebyshev filter steps (Alg. 1)                       */
+  double t_ortho_ms;         /* BCGS2 against locked + CholQR2 (Alg. 3 l. 4)          */
+  double t_rr_ms;            /* Rayleigh-Ritz + residuals + locking (ll. 5-7)          */
+  double filter_bytes;       /* algorithmic HBM bytes of the filter steps */
+} scsf_stats;
+
+/* ---------------------------------------------------------------- sort ---- */
+
+/* Workspace for scsf_sort / scsf_signatures (bytes). */
+size_t scsf_sort_workspace_bytes(int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0);
+
+/*
+ * Truncated-FFT greedy ordering, Alg. 2.
+ *  params  dev [N][F][p^dim] fp64, x fastest: the parameter matrices P^(i)
+ *          (nodal coefficient values, R7), F fields per problem (R6).
+ *  p0      truncation: modes k in [-p0/2, p0/2-1]^dim are kept (R1);
+ *          even, 2 <= p0 <= p.
+ *  start   first problem ("i_0 = 1", 0-based here).
+ *  perm    host [N] out: solve order seq_mat, a permutation of 0..N-1.
+ *  d2_best host [N-1] out or NULL: squared Frobenius distance of each greedy step.
+ *  d2_second host [N-1] out or NULL: runner-up squared distance (inf if none).
+ * Distances are compared squared (R5); ties go to the lowest index (strict `<`,
+ * P:243, R4); `dis = 1000` is read as +inf (R3).
+ * Errors: SCSF_ERR_ARG (N < 1, dim not 2/3, p0 odd or > p, start out of range).
+ */
+int scsf_sort(const double* params, int32_t N, int32_t dim, int32_t p, int32_t F,
+              int32_t p0, int32_t start, int32_t* perm, double* d2_best,
+              double* d2_second, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Alg. 2 ll. 3-5 only: sig dev [N][F*p0^dim] complex128 (interleaved re, im),
+ * C order [f][kz][ky][kx], k from -p0/2: the unnormalised DFT
+ * S[k] = sum_x P[x] exp(-2 pi i <k,x>/p) at the kept modes (R1, R2).
+ */
+int scsf_signatures(const double* params, int32_t N, int32_t dim, int32_t p, int32_t F,
+                    int32_t p0, double* sig, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ operators ---- */
+
+/*
+ * Flux-form FD assembly (App. B; reading R20):
+ *   A(k,k) = sum of the 2*dim face coefficients around node k / h^2 + c[k],
+ *   A(k,k+s_d) = -a(face between k and k+s_d) / h^2.
+ * faces_x dev [n_ops][nz][ny][nx+1], faces_y dev [n_ops][nz][ny+1][nx],
+ * faces_z dev [n_ops][nz+1][ny][nx] (dim 3, else NULL), c dev [n_ops][n]
+ * (NULL = 0); h = 1/(nx+1).  Writes ops->coef (cast away const: the caller
+ * owns it) for all n_ops operators; pads k >= n with 0.
+ */
+int scsf_assemble(const scsf_ops* ops, double h, const double* faces_x,
+                  const double* faces_y, const double* faces_z, const double* c,
+                  double* coef_out, void* stream);
+
+/* ------------------------------------------------------------- filter ---- */
+
+/*
+ * Chebyshev filter, Alg. 1 with uniform degree (R8):
+ *   A~ = (A - cI)/e, sigma_1 = e/(lambda - c), Y_1 = sigma_1 A~ Y_0,
+ *   sigma_{i+1} = 1/(2/sigma_1 - sigma_i),
+ *   Y_{i+1} = 2 sigma_{i+1} A~ Y_i - sigma_{i+1} sigma_i Y_{i-1}.
+ * Y0 dev [k][ldy] in; Ym dev [k][ldy] out (may not alias Y0).  ws: 2 blocks.
+ * Errors: SCSF_ERR_ARG (degree < 1, e <= 0, lambda == c, ldy < n).
+ */
+size_t scsf_filter_workspace_bytes(const scsf_ops* ops, int32_t k, int64_t ldy);
+int scsf_cheb_filter(const scsf_ops* ops, int32_t op_index, const double* Y0, int64_t ldy,
+                     int32_t k, int32_t degree, double lambda, double c, double e,
+                     double* Ym, void* ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------- solve ---- */
+
+/*
+ * Workspace for scsf_solve_one / scsf_solve_queue with block b = L + nex.
+ */
+size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
+
+/*
+ * ChFSI for one operator, Alg. 3: the L smallest eigenpairs of
+ * A^(op_index) to relative residual ||Av - lv||/||Av|| <= tol.
+ *  nex       extra (inherited) subspace columns: block b = L + nex (R12)
+ *  degree    Chebyshev filter degree m (default 20)
+ *  max_iter  outer-iteration cap (R24; 200)
+ *  warm_vecs dev [b][ld_vec] or NULL: initial block V~_0 ("V~_0 = V^(i-1)");
+ *            NULL = seeded Gaussian start (R17), seed + op_index.
+ *  evals     dev [b] out: Ritz values ascending; the first L are converged.
+ *  evecs     dev [b][ld_vec] out: orthonormal Ritz vectors (sign: largest |.|
+ *            entry positive, R21); may alias warm_vecs.
+ *  ld_vec    leading dimension of warm_vecs / evecs (>= n).
+ *  st        host out (may be NULL).
+ * Errors: SCSF_ERR_ARG (L < 1, nex < 0, L + nex > n, degree < 1, tol <= 0),
+ * SCSF_ERR_WORKSPACE, SCSF_ERR_NUMERICAL (not converged; outputs hold the
+ * best pairs found and st->max_rel_resid the worst residual).
+ */
+int scsf_solve_one(const scsf_ops* ops, int32_t op_index, int32_t L, int32_t nex,
+                   int32_t degree, double tol, int32_t max_iter, const double* warm_vecs,
+                   uint64_t seed, double* evals, double* evecs, int64_t ld_vec,
+                   scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * SCSF sequential solve along a sorted chain (Fig. 2 d1-d3):
+ * operator chain[0] starts from a seeded random block, every later one from
+ * the previous operator's final b-block (warm start, R11: one Rayleigh-Ritz
+ * on the new operator before the first filter).
+ *  chain   host [n_chain]: operator indices in solve order (a slice of scsf_sort's perm)
+ *  evals   dev [n_chain][L] out, by chain position
+ *  evecs   dev [n_chain][L][ld_vec] out or NULL
+ *  st      host [n_chain] out or NULL
+ * A non-converged operator is recorded in st[k].status and the chain
+ * continues; the return value is the worst status.
+ */
+int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L,
+                     int32_t nex, int32_t degree, double tol, int32_t max_iter, uint64_t seed,
+                     double* evals, double* evecs, int64_t ld_vec, scsf_stats* st,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------- helpers ---- */
+
+const char* scsf_last_error(void);   /* thread-local message for the last non-OK status */
+int scsf_abi_version(void);          /* SCSF_ABI_VERSION                                */
+int64_t scsf_launch_count(void);     /* kernels launched by this process so far         */
+int scsf_set_timing(int32_t on);     /* enable per-phase CUDA-event timers; returns the old state */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCSF_H_ */

@@ -1,0 +1,249 @@
+// api.cu — the extern "C" entry points declared in include/scsf.h:
+// argument validation, workspace carving, error strings.  All arithmetic is
+// in the k_*.cu kernels; this file only sequences them.
+#include "common.cuh"
+
+#include <atomic>
+#include <cstdarg>
+#include <cstring>
+
+namespace scsf {
+
+static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void count_launch(int n) { g_launches += n; }
+
+// k_sort.cu
+size_t sort_ws_bytes(int N, int dim, int p, int F, int p0);
+int signatures_impl(const double* params, int N, int dim, int p, int F, int p0, double2* sig, Arena& a,
+                    cudaStream_t s);
+int sort_impl(const double* params, int N, int dim, int p, int F, int p0, int start, int* perm,
+              double* d2_best, double* d2_second, Arena& a, cudaStream_t s);
+// solver.cu
+int set_timing(int on);
+// k_stencil.cu
+int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
+                  const double* c, double* coef, cudaStream_t s);
+int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
+                 int ncols, const double* fp, int step, cudaStream_t s);
+
+}  // namespace scsf
+
+#include "solver.cuh"
+
+using namespace scsf;
+
+static int check_ops(const scsf_ops* ops) {
+  SCSF_ARG_CHECK(ops != nullptr, "ops is NULL");
+  SCSF_ARG_CHECK(ops->dim == 2 || ops->dim == 3, "dim must be 2 or 3 (got %d)", ops->dim);
+  SCSF_ARG_CHECK(ops->nx >= 1 && ops->ny >= 1 && ops->nz >= 1, "grid sizes must be >= 1");
+  SCSF_ARG_CHECK(ops->dim == 3 || ops->nz == 1, "nz must be 1 when dim == 2");
+  SCSF_ARG_CHECK(ops->n_ops >= 1, "n_ops must be >= 1");
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(ops->ld >= n && ops->ld % 32 == 0, "ld must be >= n and a multiple of 32");
+  SCSF_ARG_CHECK(ops->coef != nullptr, "coef is NULL");
+  return SCSF_OK;
+}
+
+static int check_solve_args(const scsf_ops* ops, int L, int nex, int degree, double tol, int max_iter) {
+  SCSF_TRY(check_ops(ops));
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(L >= 1, "L must be >= 1");
+  SCSF_ARG_CHECK(nex >= 0, "nex must be >= 0");
+  SCSF_ARG_CHECK(L + nex <= n, "L + nex must be <= n");
+  SCSF_ARG_CHECK(L + nex <= 368, "L + nex must be <= 368 in this build");
+  SCSF_ARG_CHECK(degree >= 1, "degree must be >= 1");
+  SCSF_ARG_CHECK(tol > 0.0, "tol must be > 0");
+  SCSF_ARG_CHECK(max_iter >= 0, "max_iter must be >= 0");
+  return SCSF_OK;
+}
+
+extern "C" {
+
+const char* scsf_last_error(void) { return g_err; }
+int scsf_abi_version(void) { return SCSF_ABI_VERSION; }
+int64_t scsf_launch_count(void) { return g_launches.load(); }
+int scsf_set_timing(int32_t on) { return set_timing(on); }
+
+size_t scsf_sort_workspace_bytes(int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0) {
+  if (N < 1 || (dim != 2 && dim != 3) || p < 1 || F < 1 || p0 < 1) return 0;
+  return sort_ws_bytes(N, dim, p, F, p0);
+}
+
+static int check_sort(int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0) {
+  SCSF_ARG_CHECK(N >= 1, "N must be >= 1");
+  SCSF_ARG_CHECK(dim == 2 || dim == 3, "dim must be 2 or 3");
+  SCSF_ARG_CHECK(p >= 1 && F >= 1, "p and F must be >= 1");
+  SCSF_ARG_CHECK(p0 >= 2 && p0 % 2 == 0 && p0 <= p, "p0 must be even with 2 <= p0 <= p");
+  return SCSF_OK;
+}
+
+int scsf_signatures(const double* params, int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0,
+                    double* sig, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_sort(N, dim, p, F, p0));
+  SCSF_ARG_CHECK(params && sig, "params / sig is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  Arena a(ws, ws_bytes);
+  if (!ws) {
+    set_error("workspace is NULL");
+    return SCSF_ERR_WORKSPACE;
+  }
+  int r = signatures_impl(params, N, dim, p, F, p0, (double2*)sig, a, s);
+  if (r == SCSF_ERR_WORKSPACE) set_error("workspace too small");
+  if (r != SCSF_OK) return r;
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+int scsf_sort(const double* params, int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0, int32_t start,
+              int32_t* perm, double* d2_best, double* d2_second, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_sort(N, dim, p, F, p0));
+  SCSF_ARG_CHECK(params && perm, "params / perm is NULL");
+  SCSF_ARG_CHECK(start >= 0 && start < N, "start out of range");
+  if (!ws || ws_bytes < sort_ws_bytes(N, dim, p, F, p0)) {
+    set_error("workspace too small: need %zu bytes", sort_ws_bytes(N, dim, p, F, p0));
+    return SCSF_ERR_WORKSPACE;
+  }
+  Arena a(ws, ws_bytes);
+  return sort_impl(params, N, dim, p, F, p0, start, perm, d2_best, d2_second, a, (cudaStream_t)stream);
+}
+
+int scsf_assemble(const scsf_ops* ops, double h, const double* faces_x, const double* faces_y,
+                  const double* faces_z, const double* c, double* coef_out, void* stream) {
+  SCSF_ARG_CHECK(ops != nullptr, "ops is NULL");
+  scsf_ops o = *ops;
+  o.coef = coef_out;
+  SCSF_TRY(check_ops(&o));
+  SCSF_ARG_CHECK(faces_x && faces_y && (ops->dim == 2 || faces_z), "face arrays missing");
+  SCSF_ARG_CHECK(h > 0.0, "h must be > 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_TRY(assemble_impl(&o, h, faces_x, faces_y, faces_z, c, coef_out, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+size_t scsf_filter_workspace_bytes(const scsf_ops* ops, int32_t k, int64_t ldy) {
+  if (!ops || k < 1) return 0;
+  Arena a(nullptr, 0);
+  a.take<double>(2 * ldy * k);
+  a.take<double>(4);
+  return a.off;
+}
+
+int scsf_cheb_filter(const scsf_ops* ops, int32_t op_index, const double* Y0, int64_t ldy, int32_t k,
+                     int32_t degree, double lambda, double c, double e, double* Ym, void* ws, size_t ws_bytes,
+                     void* stream) {
+  SCSF_TRY(check_ops(ops));
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(op_index >= 0 && op_index < ops->n_ops, "op_index out of range");
+  SCSF_ARG_CHECK(Y0 && Ym && Y0 != Ym, "Y0 / Ym NULL or aliased");
+  SCSF_ARG_CHECK(k >= 1 && ldy >= n, "k >= 1 and ldy >= n required");
+  SCSF_ARG_CHECK(degree >= 1, "degree must be >= 1");
+  SCSF_ARG_CHECK(e > 0.0 && lambda != c, "need e > 0 and lambda != c");
+  Arena a(ws, ws_bytes);
+  double* B1 = a.take<double>(ldy * k);
+  double* B2 = a.take<double>(ldy * k);
+  double* fp = a.take<double>(4);
+  if (a.overflow || !ws) {
+    set_error("workspace too small");
+    return SCSF_ERR_WORKSPACE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  double hfp[4] = {lambda, c, e, 0.0};
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(fp, hfp, sizeof(hfp), cudaMemcpyHostToDevice, s));
+  // rotate over {Y0 (read-only), B1, B2, Ym}: Y_{s+1} never overwrites Y_s or Y_{s-1}
+  const double* prev = nullptr;
+  const double* cur = Y0;
+  double* bufs[3] = {B1, B2, Ym};
+  int bi = 0;
+  for (int st = 0; st < degree; ++st) {
+    double* out;
+    if (st == degree - 1) {
+      out = Ym;
+    } else {
+      out = bufs[bi % 2];   // B1 / B2 alternate
+      ++bi;
+    }
+    SCSF_TRY(stencil_impl(ops, op_index, cur, prev, out, ldy, k, fp, st, s));
+    prev = cur;
+    cur = out;
+  }
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex) {
+  if (!ops || L < 1 || nex < 0) return 0;
+  return solve_ws_bytes(ops, L, nex);
+}
+
+int scsf_solve_one(const scsf_ops* ops, int32_t op_index, int32_t L, int32_t nex, int32_t degree, double tol,
+                   int32_t max_iter, const double* warm_vecs, uint64_t seed, double* evals, double* evecs,
+                   int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(op_index >= 0 && op_index < ops->n_ops, "op_index out of range");
+  SCSF_ARG_CHECK(evals && evecs, "evals / evecs NULL");
+  SCSF_ARG_CHECK(ld_vec >= n, "ld_vec must be >= n");
+  cudaStream_t s = (cudaStream_t)stream;
+  SolveWS w;
+  SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w));
+  const int b = L + nex;
+  if (warm_vecs) {
+    SCSF_CUDA_CHECK(cudaMemcpy2DAsync(w.V, w.ldv * sizeof(double), warm_vecs, ld_vec * sizeof(double),
+                                      n * sizeof(double), b, cudaMemcpyDeviceToDevice, s));
+    if (w.ldv > n)
+      SCSF_CUDA_CHECK(cudaMemset2DAsync(w.V + n, w.ldv * sizeof(double), 0, (w.ldv - n) * sizeof(double), b, s));
+  }
+  int r = solve_core(ops, op_index, L, nex, degree, tol, max_iter, warm_vecs != nullptr, true,
+                     seed + (uint64_t)op_index, w, st, s);
+  if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(evals, w.theta_sorted, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  SCSF_CUDA_CHECK(cudaMemcpy2DAsync(evecs, ld_vec * sizeof(double), w.V, w.ldv * sizeof(double),
+                                    n * sizeof(double), b, cudaMemcpyDeviceToDevice, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return r;
+}
+
+int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
+                     int32_t degree, double tol, int32_t max_iter, uint64_t seed, double* evals, double* evecs,
+                     int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(n_chain >= 0, "n_chain must be >= 0");
+  SCSF_ARG_CHECK(n_chain == 0 || chain != nullptr, "chain is NULL");
+  SCSF_ARG_CHECK(n_chain == 0 || evals != nullptr, "evals is NULL");
+  SCSF_ARG_CHECK(evecs == nullptr || ld_vec >= n, "ld_vec must be >= n");
+  for (int k = 0; k < n_chain; ++k)
+    SCSF_ARG_CHECK(chain[k] >= 0 && chain[k] < ops->n_ops, "chain[%d]=%d out of range", k, chain[k]);
+  if (n_chain == 0) return SCSF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  SolveWS w;
+  SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w));
+  int worst = SCSF_OK;
+  for (int k = 0; k < n_chain; ++k) {
+    scsf_stats local{};
+    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0, false, seed + (uint64_t)chain[k],
+                       w, &local, s);
+    if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
+    if (r > worst) worst = r;
+    if (st) st[k] = local;
+    SCSF_CUDA_CHECK(cudaMemcpyAsync(evals + (int64_t)k * L, w.theta_sorted, L * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+    if (evecs)
+      SCSF_CUDA_CHECK(cudaMemcpy2DAsync(evecs + (int64_t)k * L * ld_vec, ld_vec * sizeof(double), w.V,
+                                        w.ldv * sizeof(double), n * sizeof(double), L, cudaMemcpyDeviceToDevice,
+                                        s));
+  }
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return worst;
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// k_stencil.cu — operator-side kernels: FD assembly, Gershgorin bound, the
+// fused Chebyshev three-term-recurrence SpMM step (Alg. 1)
+// and the column residual norms of Alg. 3 l. 7 (metric P:844).
+//
+// A is a symmetric 5-/7-point stencil in DIA form (include/scsf.h).  One
+// filter step is
+//   Y_{s+1} = a_s (A - cI) Y_s + b_s Y_{s-1},
+//   a_0 = sigma_1/e, b_0 = 0;  a_s = 2 sigma_{s+1}/e, b_s = -sigma_{s+1} sigma_s,
+// i.e. Alg. 1's  Y_{i+1} = 2 sigma_{i+1} A~ Y_i - sigma_{i+1} sigma_i Y_{i-1}
+// with A~ = (A - cI)/e folded into the scalars.  The sigma recurrence is
+// evaluated on the device from (lambda, c, e) so the host never syncs for it.
+// HBM roofline: per point and column 8 B read Y_s, 8 B read Y_{s-1}, 8 B write
+// Y_{s+1}; coefficient arrays (8(1+dim) B per point) are shared by all columns
+// and stay L2-resident.
+#include "common.cuh"
+
+namespace scsf {
+
+// ------------------------------------------------------------- assembly ----
+__global__ void k_assemble(int dim, int nx, int ny, int nz, int n_ops, int64_t ld, double inv_h2,
+                           const double* __restrict__ fx, const double* __restrict__ fy,
+                           const double* __restrict__ fz, const double* __restrict__ c,
+                           double* __restrict__ coef) {
+  int64_t n = (int64_t)nx * ny * nz;
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int op = blockIdx.y;
+  if (idx >= ld) return;
+  double* out = coef + (int64_t)op * (1 + dim) * ld;
+  if (idx >= n) {
+    for (int d = 0; d <= dim; ++d) out[d * ld + idx] = 0.0;
+    return;
+  }
+  int i = (int)(idx % nx);
+  int j = (int)((idx / nx) % ny);
+  int l = (int)(idx / ((int64_t)nx * ny));
+  const double* ax = fx + (int64_t)op * nz * ny * (nx + 1);
+  const double* ay = fy + (int64_t)op * nz * (ny + 1) * nx;
+  double axl = ax[((int64_t)l * ny + j) * (nx + 1) + i];
+  double axr = ax[((int64_t)l * ny + j) * (nx + 1) + i + 1];
+  double ayl = ay[((int64_t)l * (ny + 1) + j) * nx + i];
+  double ayr = ay[((int64_t)l * (ny + 1) + j + 1) * nx + i];
+  double diag = axl + axr + ayl + ayr;
+  double czv = 0.0, azr = 0.0;
+  if (dim == 3) {
+    const double* az = fz + (int64_t)op * (nz + 1) * ny * nx;
+    double azl = az[((int64_t)l * ny + j) * nx + i];
+    azr = az[((int64_t)(l + 1) * ny + j) * nx + i];
+    diag += azl + azr;
+    czv = (l < nz - 1) ? -azr * inv_h2 : 0.0;
+  }
+  diag = diag * inv_h2 + (c ? c[(int64_t)op * n + idx] : 0.0);
+  out[idx] = diag;
+  out[ld + idx] = (i < nx - 1) ? -axr * inv_h2 : 0.0;
+  out[2 * ld + idx] = (j < ny - 1) ? -ayr * inv_h2 : 0.0;
+  if (dim == 3) out[3 * ld + idx] = czv;
+}
+
+// ------------------------------------------------------------ Gershgorin ----
+// beta = max_k sum_j |A(k, j)| (reading R10).  Non-negative doubles order like
+// their bit patterns, so an integer atomicMax is exact and order-independent.
+__global__ void k_gershgorin(const double* __restrict__ cf, int dim, int nx, int ny, int64_t n,
+                             int64_t ld, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  const int64_t sxy = (int64_t)nx * ny;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double r = fabs(cf[k]) + fabs(cf[ld + k]) + fabs(cf[2 * ld + k]);
+    if (k >= 1) r += fabs(cf[ld + k - 1]);
+    if (k >= nx) r += fabs(cf[2 * ld + k - nx]);
+    if (dim == 3) {
+      r += fabs(cf[3 * ld + k]);
+      if (k >= sxy) r += fabs(cf[3 * ld + k - sxy]);
+    }
+    m = fmax(m, r);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// ---------------------------------------------------- filter / SpMM step ----
+// fp = {lambda, c, e} (device).  step < 0: plain SpMM  Out = A X.
+__device__ __forceinline__ void step_scalars(const double* fp, int step, double& a, double& b,
+                                             double& c) {
+  if (step < 0) {
+    a = 1.0; b = 0.0; c = 0.0;
+    return;
+  }
+  double lam = fp[0], cc = fp[1], e = fp[2];
+  double s1 = e / (lam - cc);
+  c = cc;
+  if (step == 0) {
+    a = s1 / e; b = 0.0;
+    return;
+  }
+  double sig = s1, prev = s1;
+  for (int i = 1; i <= step; ++i) {     // sigma_{i+1} = 1 / (2/sigma_1 - sigma_i)
+    prev = sig;
+    sig = 1.0 / (2.0 / s1 - sig);
+  }
+  a = 2.0 * sig / e;
+  b = -sig * prev;
+}
+
+constexpr int ST_THREADS = 256;
+constexpr int ST_COLS = 8;     // columns per CTA sharing the coefficient registers
+
+template <int DIM>
+__global__ void __launch_bounds__(ST_THREADS) k_stencil(
+    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n,
+    const double* __restrict__ X, const double* Xp, double* Out,   // Out may alias Xp (same-index read-then-write)
+    int64_t ldv, int ncols, const double* __restrict__ fp, int step) {
+  int64_t k = (int64_t)blockIdx.x * ST_THREADS + threadIdx.x;
+  if (k >= n) return;
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int64_t sxy = (int64_t)nx * ny;
+  const double dg = cf[k] - c;
+  const double xp = cf[ldc + k];
+  const double xm = (k >= 1) ? cf[ldc + k - 1] : 0.0;
+  const double yp = cf[2 * ldc + k];
+  const double ym = (k >= nx) ? cf[2 * ldc + k - nx] : 0.0;
+  double zp = 0.0, zm = 0.0;
+  if (DIM == 3) {
+    zp = cf[3 * ldc + k];
+    zm = (k >= sxy) ? cf[3 * ldc + k - sxy] : 0.0;
+  }
+  const bool hp = k + 1 < n, hm = k >= 1, hyp = k + nx < n, hym = k >= nx;
+  const bool hzp = (DIM == 3) && (k + sxy < n), hzm = (DIM == 3) && (k >= sxy);
+  int j0 = blockIdx.y * ST_COLS;
+  int j1 = min(ncols, j0 + ST_COLS);
+  for (int j = j0; j < j1; ++j) {
+    const double* x = X + (int64_t)j * ldv;
+    double v = dg * x[k];
+    if (hp) v = fma(xp, x[k + 1], v);
+    if (hm) v = fma(xm, x[k - 1], v);
+    if (hyp) v = fma(yp, x[k + nx], v);
+    if (hym) v = fma(ym, x[k - nx], v);
+    if (DIM == 3) {
+      if (hzp) v = fma(zp, x[k + sxy], v);
+      if (hzm) v = fma(zm, x[k - sxy], v);
+    }
+    v *= a;
+    if (b != 0.0) v = fma(b, Xp[(int64_t)j * ldv + k], v);
+    Out[(int64_t)j * ldv + k] = v;
+  }
+}
+
+// ---------------------------------------------------------- residuals ----
+// For active column j: res[j] = ||W_j - theta_j V_j||_2, wn[j] = ||W_j||_2 (fixed-order sums).
+__global__ void __launch_bounds__(256) k_resid(const double* __restrict__ V, const double* __restrict__ W,
+                                               int64_t ldv, int64_t n, const double* __restrict__ theta,
+                                               double* __restrict__ res, double* __restrict__ wn) {
+  int j = blockIdx.x;
+  const double* v = V + (int64_t)j * ldv;
+  const double* w = W + (int64_t)j * ldv;
+  double th = theta[j];
+  double r2 = 0.0, w2 = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    double wk = w[k];
+    double d = fma(-th, v[k], wk);
+    r2 = fma(d, d, r2);
+    w2 = fma(wk, wk, w2);
+  }
+  __shared__ double sr[8], sw[8];
+  r2 = warp_sum(r2);
+  w2 = warp_sum(w2);
+  if ((threadIdx.x & 31) == 0) {
+    sr[threadIdx.x >> 5] = r2;
+    sw[threadIdx.x >> 5] = w2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      a += sr[i];
+      b += sw[i];
+    }
+    res[j] = sqrt(a);
+    wn[j] = sqrt(b);
+  }
+}
+
+// ------------------------------------------------------------------ host ----
+int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy,
+                  const double* fz, const double* c, double* coef, cudaStream_t s) {
+  dim3 g(ceil_div(ops->ld, 256), ops->n_ops);
+  k_assemble<<<g, 256, 0, s>>>(ops->dim, ops->nx, ops->ny, ops->nz, ops->n_ops, ops->ld,
+                               1.0 / (h * h), fx, fy, fz, c, coef);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s) {
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  SCSF_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
+  int blocks = min(ceil_div(n, 256), 148 * 4);
+  k_gershgorin<<<blocks, 256, 0, s>>>(cf, ops->dim, ops->nx, ops->ny, n, ops->ld, out);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+// Out[:, 0:ncols] = step-th filter update (or A X when step < 0).
+int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out,
+                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s) {
+  if (ncols <= 0) return SCSF_OK;
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  dim3 g(ceil_div(n, ST_THREADS), ceil_div(ncols, ST_COLS));
+  if (ops->dim == 2)
+    k_stencil<2><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+  else
+    k_stencil<3><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
+               const double* theta, double* res, double* wn, cudaStream_t s) {
+  if (ncols <= 0) return SCSF_OK;
+  k_resid<<<ncols, 256, 0, s>>>(V, W, ldv, n, theta, res, wn);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+}  // namespace scsf

@@ -1,0 +1,264 @@
+// solver.cu — ChFSI driver, Alg. 3, and the SCSF chain
+// (Fig. 2 d1-d3; warm start P:270-277).
+//
+// Block layout: V, W = AV, T1, T2 are n x b column-major blocks (ld = n
+// rounded up to 32).  Columns [0, kL) of V are locked Ritz vectors (ascending
+// Ritz values), columns [kL, b) are active.  Per outer iteration:
+//   1. filter   Y_m = C_m(V_act)             Alg. 1, m stencil steps
+//   2. BCGS2    Y <- Y - V_L (V_L^T Y), x2   orthogonality to locked (R14)
+//   3. CholQR2  Y = Q R, two passes          l. 4 (R13)
+//   4. RR       W = AQ, G = Q^T W, G = Z T Z^T, V_act <- QZ, W <- WZ   ll. 5-6
+//   5. resid    ||W_j - t_j V_j|| / ||W_j||
+//   6. lock     contiguous run from kL (R15); next (lambda, c, e) (R9)
+// The host reads the device control block once per iteration (kL drives the
+// launch shapes of the next iteration).
+#include "solver.cuh"
+
+#include <algorithm>
+#include <utility>
+
+namespace scsf {
+
+// kernels (k_*.cu)
+int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out,
+                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s);
+int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
+               const double* theta, double* res, double* wn, cudaStream_t s);
+int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s);
+int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, int b2, int64_t n,
+            double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s);
+int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+            double alpha, double beta, double* Out, int64_t ldo, cudaStream_t s);
+size_t tn_partial_doubles(int64_t n, int b1, int b2);
+int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
+                  Ctrl* ctrl, cudaStream_t s);
+int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
+                double* Zout, Ctrl* ctrl, cudaStream_t s);
+int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
+              double tol, Ctrl* ctrl, double* fp, cudaStream_t s);
+int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
+int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, cudaStream_t s);
+int finalize_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
+                  const double* V, int64_t ldv, int64_t n, double* Out, int64_t ldo, Ctrl* ctrl,
+                  cudaStream_t s);
+
+static void carve(Arena& a, SolveWS& w, int64_t n, int b) {
+  w.n = n;
+  w.b = b;
+  w.ldv = round_up(n, 32);
+  w.V = a.take<double>(w.ldv * b);
+  w.W = a.take<double>(w.ldv * b);
+  w.T1 = a.take<double>(w.ldv * b);
+  w.T2 = a.take<double>(w.ldv * b);
+  const int64_t bb = (int64_t)b * b;
+  w.S = a.take<double>(bb);
+  w.Rinv = a.take<double>(bb);
+  w.Zs = a.take<double>(bb);
+  w.Zwork = a.take<double>(bb);
+  w.Gwork = a.take<double>(bb);
+  w.C = a.take<double>(bb);
+  w.P = a.take<double>((int64_t)tn_partial_doubles(n, b, b));
+  w.theta = a.take<double>(b);
+  w.theta_sorted = a.take<double>(b);
+  w.res = a.take<double>(b);
+  w.wn = a.take<double>(b);
+  w.rel = a.take<double>(b);
+  w.fp = a.take<double>(4);
+  w.perm = a.take<int>(b);
+  w.ctrl = a.take<Ctrl>(1);
+  w.gersh = a.take<unsigned long long>(1);
+}
+
+size_t solve_ws_bytes(const scsf_ops* ops, int L, int nex) {
+  Arena a(nullptr, 0);
+  SolveWS w;
+  carve(a, w, (int64_t)ops->nx * ops->ny * ops->nz, L + nex);
+  return a.off;
+}
+
+int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_bytes, SolveWS& w) {
+  Arena a(ws, ws_bytes);
+  carve(a, w, (int64_t)ops->nx * ops->ny * ops->nz, L + nex);
+  if (a.overflow || ws == nullptr) {
+    set_error("workspace too small: need %zu bytes, got %zu", a.off, ws_bytes);
+    return SCSF_ERR_WORKSPACE;
+  }
+  return SCSF_OK;
+}
+
+// Q = CholQR pass on columns [0, ncols) of Y (in place, or into Out when Out != Y).
+static int cholqr_pass(SolveWS& w, double* Y, double* Out, int ncols, cudaStream_t s) {
+  SCSF_TRY(gemm_tn(Y, w.ldv, ncols, Y, w.ldv, ncols, w.n, 1.0, 1, w.S, ncols, w.P, s));
+  SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n, w.Rinv, w.Gwork, w.ctrl, s));
+  SCSF_TRY(gemm_nn(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, s));
+  return SCSF_OK;
+}
+
+// Rayleigh-Ritz on block columns [k0, b): W = AV, G = V^T W, rotate V and W,
+// residual norms, locking.
+static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L, double tol,
+                         int64_t& spmm_cols, cudaStream_t s) {
+  const int ba = w.b - k0;
+  double* Va = w.V + (int64_t)k0 * w.ldv;
+  double* Wa = w.W + (int64_t)k0 * w.ldv;
+  SCSF_TRY(stencil_impl(ops, op, Va, nullptr, Wa, w.ldv, ba, w.fp, -1, s));
+  spmm_cols += ba;
+  SCSF_TRY(gemm_tn(Va, w.ldv, ba, Wa, w.ldv, ba, w.n, 1.0, 1, w.S, ba, w.P, s));
+  SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
+  SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Va, w.ldv, s));
+  SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
+  SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
+  return SCSF_OK;
+}
+
+// ---- optional phase timers (scsf_set_timing) ----
+static int g_timing = 0;
+int set_timing(int on) {
+  int old = g_timing;
+  g_timing = on ? 1 : 0;
+  return old;
+}
+
+struct PhaseTimer {
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool on = false;
+  double filter = 0, ortho = 0, rr = 0;
+  int init() {
+    on = g_timing != 0;
+    if (!on) return SCSF_OK;
+    for (auto& e : ev) SCSF_CUDA_CHECK(cudaEventCreate(&e));
+    return SCSF_OK;
+  }
+  int mark(int i, cudaStream_t s) {
+    if (on) SCSF_CUDA_CHECK(cudaEventRecord(ev[i], s));
+    return SCSF_OK;
+  }
+  // call after a stream sync that follows mark(3)
+  int accumulate() {
+    if (!on) return SCSF_OK;
+    float a = 0, b = 0, c = 0;
+    SCSF_CUDA_CHECK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    SCSF_CUDA_CHECK(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    SCSF_CUDA_CHECK(cudaEventElapsedTime(&c, ev[2], ev[3]));
+    filter += a;
+    ortho += b;
+    rr += c;
+    return SCSF_OK;
+  }
+  ~PhaseTimer() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+static int read_ctrl(const SolveWS& w, Ctrl& h, cudaStream_t s) {
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(&h, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+static int clear_chol_flag(SolveWS& w, cudaStream_t s) {
+  SCSF_CUDA_CHECK(cudaMemsetAsync(&w.ctrl->chol_fail, 0, sizeof(int32_t), s));
+  return SCSF_OK;
+}
+
+// Solve operator `op`.  warm: V already holds the initial b-block (orthonormal).
+// On return w.V holds the final block sorted ascending with the sign convention,
+// w.theta_sorted the Ritz values.
+int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double tol, int max_iter,
+               bool warm, bool orthonormalize, uint64_t seed, SolveWS& w, scsf_stats* st, cudaStream_t s) {
+  const int b = L + nex;
+  int64_t spmm_cols = 0;
+  int filter_steps = 0, iters = 0;
+  double filter_bytes = 0.0;
+  const double coef_bytes = 8.0 * (1 + ops->dim) * (double)w.n;
+  PhaseTimer tm;
+  SCSF_TRY(tm.init());
+  Ctrl h{};
+  SCSF_TRY(gershgorin_impl(ops, op, w.gersh, s));
+  SCSF_TRY(ctrl_init_impl(w.ctrl, w.gersh, s));
+  if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, s));
+  if (!warm || orthonormalize) {
+    SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
+    SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
+  }
+  // one Rayleigh-Ritz of the new operator on the initial block (R11)
+  SCSF_TRY(rayleigh_ritz(ops, op, w, 0, L, tol, spmm_cols, s));
+  SCSF_TRY(read_ctrl(w, h, s));
+  int kL = h.kL;
+  int fallbacks = 0;
+  while (kL < L && iters < max_iter && !(h.nonfinite & 1)) {
+    ++iters;
+    const int ba = b - kL;
+    double* y[3] = {w.V + (int64_t)kL * w.ldv, w.T1 + (int64_t)kL * w.ldv, w.T2 + (int64_t)kL * w.ldv};
+    // 1. Chebyshev filter (Alg. 1) on the active block
+    SCSF_TRY(tm.mark(0, s));
+    SCSF_TRY(stencil_impl(ops, op, y[0], nullptr, y[1], w.ldv, ba, w.fp, 0, s));
+    for (int st_i = 1; st_i < degree; ++st_i)
+      SCSF_TRY(stencil_impl(ops, op, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], w.ldv, ba, w.fp,
+                            st_i, s));
+    double* F = y[degree % 3];
+    SCSF_TRY(tm.mark(1, s));
+    // algorithmic bytes: first step reads Y0 + writes Y1, later steps read Y_s, Y_{s-1}
+    // and write Y_{s+1}; one pass over the coefficient arrays per step
+    filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * ba * (degree - 1) + coef_bytes * degree;
+    filter_steps += degree;
+    spmm_cols += (int64_t)degree * ba;
+    // 2. block classical Gram-Schmidt, twice, against the locked vectors
+    if (kL > 0) {
+      for (int rep = 0; rep < 2; ++rep) {
+        SCSF_TRY(gemm_tn(w.V, w.ldv, kL, F, w.ldv, ba, w.n, 1.0, 0, w.C, kL, w.P, s));
+        SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kL, w.C, kL, ba, -1.0, 1.0, F, w.ldv, s));
+      }
+    }
+    // 3. CholQR2 (second pass lands the block in V's active columns)
+    SCSF_TRY(clear_chol_flag(w, s));
+    SCSF_TRY(cholqr_pass(w, F, F, ba, s));
+    SCSF_TRY(cholqr_pass(w, F, y[0], ba, s));
+    SCSF_TRY(tm.mark(2, s));
+    // 4.-6. Rayleigh-Ritz, residuals, locking
+    SCSF_TRY(rayleigh_ritz(ops, op, w, kL, L, tol, spmm_cols, s));
+    SCSF_TRY(tm.mark(3, s));
+    SCSF_TRY(read_ctrl(w, h, s));
+    SCSF_TRY(tm.accumulate());
+    if (h.chol_fail) {
+      // shifted CholQR was needed: one more CholQR pass, then redo the RR step
+      ++fallbacks;
+      SCSF_CUDA_CHECK(cudaMemcpyAsync(&w.ctrl->kL, &kL, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      SCSF_TRY(clear_chol_flag(w, s));
+      SCSF_TRY(cholqr_pass(w, y[0], y[0], ba, s));
+      SCSF_TRY(rayleigh_ritz(ops, op, w, kL, L, tol, spmm_cols, s));
+      SCSF_TRY(read_ctrl(w, h, s));
+    }
+    kL = h.kL;
+  }
+  // final ascending order + sign convention into T1, then swap so V holds it
+  SCSF_TRY(finalize_impl(w.theta, w.rel, b, L, w.perm, w.theta_sorted, w.V, w.ldv, w.n, w.T1, w.ldv,
+                         w.ctrl, s));
+  std::swap(w.V, w.T1);
+  SCSF_TRY(read_ctrl(w, h, s));
+  int status = SCSF_OK;
+  if (kL < L || (h.nonfinite & 1)) status = SCSF_ERR_NUMERICAL;
+  if (st) {
+    st->status = status;
+    st->iterations = iters;
+    st->filter_steps = filter_steps;
+    st->cholqr_fallbacks = fallbacks;
+    st->n_locked = kL;
+    st->warm = warm ? 1 : 0;
+    st->spmm_columns = spmm_cols;
+    st->max_rel_resid = h.max_rel;
+    st->beta = h.beta;
+    st->t_filter_ms = tm.filter;
+    st->t_ortho_ms = tm.ortho;
+    st->t_rr_ms = tm.rr;
+    st->filter_bytes = filter_bytes;
+  }
+  if (status != SCSF_OK)
+    set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op,
+              kL, L, iters, h.max_rel);
+  return status;
+}
+
+}  // namespace scsf

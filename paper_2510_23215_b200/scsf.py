@@ -1,0 +1,273 @@
+"""Thin ctypes binding of libscsf.so (include/scsf.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module
+allocates device memory with torch, passes raw pointers and the current CUDA
+stream, and converts status codes to exceptions.  There is no CPU fallback:
+if the shared library is missing, or no CUDA device is present, the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libscsf.so")
+
+SCSF_OK, SCSF_ERR_ARG, SCSF_ERR_NUMERICAL, SCSF_ERR_DEVICE, SCSF_ERR_NOT_IMPLEMENTED, SCSF_ERR_WORKSPACE = range(6)
+_STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NUMERICAL", 3: "ERR_DEVICE", 4: "ERR_NOT_IMPLEMENTED", 5: "ERR_WORKSPACE"}
+
+EXPORTED = [
+    "scsf_sort_workspace_bytes", "scsf_sort", "scsf_signatures", "scsf_assemble",
+    "scsf_filter_workspace_bytes", "scsf_cheb_filter", "scsf_solve_workspace_bytes",
+    "scsf_solve_one", "scsf_solve_queue", "scsf_last_error", "scsf_abi_version",
+    "scsf_launch_count", "scsf_set_timing",
+]
+
+
+class ScsfError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"scsf {_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class NotConverged(ScsfError):
+    pass
+
+
+class scsf_ops(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("nz", ctypes.c_int32), ("n_ops", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("ld", ctypes.c_int64), ("coef", ctypes.c_void_p)]
+
+
+class scsf_stats(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("filter_steps", ctypes.c_int32), ("cholqr_fallbacks", ctypes.c_int32),
+                ("n_locked", ctypes.c_int32), ("warm", ctypes.c_int32),
+                ("spmm_columns", ctypes.c_int64), ("max_rel_resid", ctypes.c_double),
+                ("beta", ctypes.c_double), ("t_filter_ms", ctypes.c_double), ("t_ortho_ms", ctypes.c_double),
+                ("t_rr_ms", ctypes.c_double), ("filter_bytes", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libscsf.so; raise loudly if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libscsf.so not found at {path}: run `python -m paper_2510_23215_b200.build`")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, D, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+    OPS = ctypes.POINTER(scsf_ops)
+    ST = ctypes.POINTER(scsf_stats)
+    sig = {
+        "scsf_sort_workspace_bytes": (SZ, [I32, I32, I32, I32, I32]),
+        "scsf_sort": (ctypes.c_int, [P, I32, I32, I32, I32, I32, I32, P, P, P, P, SZ, P]),
+        "scsf_signatures": (ctypes.c_int, [P, I32, I32, I32, I32, I32, P, P, SZ, P]),
+        "scsf_assemble": (ctypes.c_int, [OPS, D, P, P, P, P, P, P]),
+        "scsf_filter_workspace_bytes": (SZ, [OPS, I32, I64]),
+        "scsf_cheb_filter": (ctypes.c_int, [OPS, I32, P, I64, I32, I32, D, D, D, P, P, SZ, P]),
+        "scsf_solve_workspace_bytes": (SZ, [OPS, I32, I32]),
+        "scsf_solve_one": (ctypes.c_int, [OPS, I32, I32, I32, I32, D, I32, P, ctypes.c_uint64, P, P, I64, ST,
+                                          P, SZ, P]),
+        "scsf_solve_queue": (ctypes.c_int, [OPS, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P, I64, ST,
+                                            P, SZ, P]),
+        "scsf_last_error": (ctypes.c_char_p, []),
+        "scsf_abi_version": (ctypes.c_int, []),
+        "scsf_launch_count": (ctypes.c_int64, []),
+        "scsf_set_timing": (ctypes.c_int, [I32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(code: int):
+    if code == SCSF_OK:
+        return
+    msg = load_library().scsf_last_error().decode(errors="replace")
+    if code == SCSF_ERR_NUMERICAL:
+        raise NotConverged(code, msg)
+    raise ScsfError(code, msg)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _require_cuda_f64(t: torch.Tensor, name: str):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def launch_count() -> int:
+    return int(load_library().scsf_launch_count())
+
+
+def set_timing(on: bool) -> bool:
+    """Enable the library's per-phase CUDA-event timers (stats t_*_ms); returns the old state."""
+    return bool(load_library().scsf_set_timing(1 if on else 0))
+
+
+def ld_for(n: int) -> int:
+    return (n + 31) // 32 * 32
+
+
+# ------------------------------------------------------------------ operators ----
+@dataclass
+class Operators:
+    """A device batch of symmetric DIA stencils (include/scsf.h `scsf_ops`)."""
+    dim: int
+    nx: int
+    ny: int
+    nz: int
+    n_ops: int
+    ld: int
+    coef: torch.Tensor          # [n_ops, 1+dim, ld] float64 on the device
+
+    @property
+    def n(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def c_struct(self) -> scsf_ops:
+        return scsf_ops(self.dim, self.nx, self.ny, self.nz, self.n_ops, 0, self.ld, self.coef.data_ptr())
+
+
+def assemble(dim: int, nx: int, h: float, faces, c: torch.Tensor | None) -> Operators:
+    """Flux-form FD assembly on the device (scsf_assemble).  faces: list of dim tensors."""
+    lib = load_library()
+    for i, f in enumerate(faces):
+        _require_cuda_f64(f, f"faces[{i}]")
+    n_ops = faces[0].shape[0]
+    n = nx ** dim
+    ld = ld_for(n)
+    nz = nx if dim == 3 else 1
+    coef = torch.empty((n_ops, 1 + dim, ld), dtype=torch.float64, device=faces[0].device)
+    ops = Operators(dim, nx, nx, nz, n_ops, ld, coef)
+    st = ops.c_struct()
+    if c is not None:
+        _require_cuda_f64(c, "c")
+    fz = faces[2] if dim == 3 else None
+    _check(lib.scsf_assemble(ctypes.byref(st), h, _ptr(faces[0]), _ptr(faces[1]), _ptr(fz), _ptr(c),
+                             _ptr(coef), _stream()))
+    return ops
+
+
+# ----------------------------------------------------------------------- sort ----
+def signatures(params: torch.Tensor, dim: int, p: int, p0: int) -> torch.Tensor:
+    """Alg. 2 ll. 3-5: truncated DFT signatures, complex128 [N, F*p0^dim]."""
+    lib = load_library()
+    _require_cuda_f64(params, "params")
+    N, F = params.shape[0], params.shape[1]
+    ws = _workspace(lib.scsf_sort_workspace_bytes(N, dim, p, F, p0), params.device)
+    sig = torch.empty((N, F * p0 ** dim, 2), dtype=torch.float64, device=params.device)
+    _check(lib.scsf_signatures(_ptr(params), N, dim, p, F, p0, _ptr(sig), _ptr(ws), ws.numel(), _stream()))
+    return torch.view_as_complex(sig)
+
+
+def sort(params: torch.Tensor, dim: int, p: int, p0: int, start: int = 0):
+    """Alg. 2: returns (perm int32[N], d2_best[N-1], d2_second[N-1]) as numpy arrays."""
+    lib = load_library()
+    _require_cuda_f64(params, "params")
+    N, F = params.shape[0], params.shape[1]
+    ws = _workspace(lib.scsf_sort_workspace_bytes(N, dim, p, F, p0), params.device)
+    perm = np.empty(N, dtype=np.int32)
+    best = np.empty(max(N - 1, 1), dtype=np.float64)
+    second = np.empty(max(N - 1, 1), dtype=np.float64)
+    _check(lib.scsf_sort(_ptr(params), N, dim, p, F, p0, start, perm.ctypes.data_as(ctypes.c_void_p),
+                         best.ctypes.data_as(ctypes.c_void_p), second.ctypes.data_as(ctypes.c_void_p),
+                         _ptr(ws), ws.numel(), _stream()))
+    return perm, best[:N - 1], second[:N - 1]
+
+
+# --------------------------------------------------------------------- filter ----
+def cheb_filter(ops: Operators, op_index: int, Y0: torch.Tensor, degree: int, lam: float, c: float,
+                e: float) -> torch.Tensor:
+    """Alg. 1 on a block Y0 [k, ldy] (column-major n x k); returns Y_m of the same shape."""
+    lib = load_library()
+    _require_cuda_f64(Y0, "Y0")
+    k, ldy = Y0.shape
+    st = ops.c_struct()
+    ws = _workspace(lib.scsf_filter_workspace_bytes(ctypes.byref(st), k, ldy), Y0.device)
+    Ym = torch.empty_like(Y0)
+    _check(lib.scsf_cheb_filter(ctypes.byref(st), op_index, _ptr(Y0), ldy, k, degree, lam, c, e, _ptr(Ym),
+                                _ptr(ws), ws.numel(), _stream()))
+    return Ym
+
+
+# ---------------------------------------------------------------------- solve ----
+def solve_workspace(ops: Operators, L: int, nex: int) -> torch.Tensor:
+    lib = load_library()
+    st = ops.c_struct()
+    return _workspace(lib.scsf_solve_workspace_bytes(ctypes.byref(st), L, nex), ops.coef.device)
+
+
+def solve_one(ops: Operators, op_index: int, L: int, nex: int, degree: int = 20, tol: float = 1e-8,
+              max_iter: int = 200, warm: torch.Tensor | None = None, seed: int = 0, raise_on_fail=True,
+              ws: torch.Tensor | None = None):
+    """Alg. 3 on one operator.  Returns (evals[b], evecs[b, ld], stats dict)."""
+    lib = load_library()
+    b = L + nex
+    st = ops.c_struct()
+    if ws is None:
+        ws = solve_workspace(ops, L, nex)
+    evals = torch.empty(b, dtype=torch.float64, device=ops.coef.device)
+    evecs = torch.empty((b, ops.ld), dtype=torch.float64, device=ops.coef.device)
+    if warm is not None:
+        _require_cuda_f64(warm, "warm")
+        assert warm.shape == (b, ops.ld)
+    stats = scsf_stats()
+    code = lib.scsf_solve_one(ctypes.byref(st), op_index, L, nex, degree, tol, max_iter, _ptr(warm),
+                              ctypes.c_uint64(seed), _ptr(evals), _ptr(evecs), ops.ld, ctypes.byref(stats),
+                              _ptr(ws), ws.numel(), _stream())
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return evals, evecs, stats.as_dict()
+
+
+def solve_queue(ops: Operators, chain, L: int, nex: int, degree: int = 20, tol: float = 1e-8,
+                max_iter: int = 200, seed: int = 0, want_vecs: bool = True, raise_on_fail=True,
+                ws: torch.Tensor | None = None, evals: torch.Tensor | None = None,
+                evecs: torch.Tensor | None = None):
+    """SCSF chain solve.  Returns (evals[n_chain, L], evecs[n_chain, L, ld] or None, stats list)."""
+    lib = load_library()
+    chain = np.ascontiguousarray(np.asarray(chain, dtype=np.int32))
+    nc = int(chain.shape[0])
+    st = ops.c_struct()
+    if ws is None:
+        ws = solve_workspace(ops, L, nex)
+    dev = ops.coef.device
+    if evals is None:
+        evals = torch.empty((nc, L), dtype=torch.float64, device=dev)
+    if want_vecs and evecs is None:
+        evecs = torch.empty((nc, L, ops.ld), dtype=torch.float64, device=dev)
+    stats = (scsf_stats * max(nc, 1))()
+    code = lib.scsf_solve_queue(ctypes.byref(st), chain.ctypes.data_as(ctypes.c_void_p), nc, L, nex, degree,
+                                tol, max_iter, ctypes.c_uint64(seed), _ptr(evals),
+                                _ptr(evecs) if want_vecs else None, ops.ld, stats, _ptr(ws), ws.numel(),
+                                _stream())
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return evals, (evecs if want_vecs else None), [stats[i].as_dict() for i in range(nc)]

@@ -82,7 +82,7 @@ class OperatorFields:
 
     @property
     def n_ops(self) -> int:
-        return self.c.shape[0]
+        return self.params.shape[0]
 
     @property
     def n(self) -> int:
@@ -122,9 +122,18 @@ def make_fields(cfg: Config, i: int, f: int, cfg_index: int | None = None):
     return g_node, g_face
 
 
-def make_batch(cfg: Config, n_ops: int | None = None, start: int = 0) -> OperatorFields:
-    """Operators start..start+n_ops-1 of config `cfg` (seeded, deterministic)."""
-    N = cfg.n_ops if n_ops is None else n_ops
+def make_batch(cfg: Config, n_ops: int | None = None, start: int = 0, indices=None,
+               params_only: bool = False) -> OperatorFields:
+    """Operators start..start+n_ops-1 (or the given global `indices`) of config `cfg`.
+
+    Operator i is a pure function of (cfg, i): seeded, deterministic.
+    params_only: skip the face/reaction arrays (the sort needs only P).
+    """
+    if indices is None:
+        N = cfg.n_ops if n_ops is None else n_ops
+        indices = range(start, start + N)
+    indices = [int(i) for i in indices]
+    N = len(indices)
     dim, nx = cfg.dim, cfg.nx
     n = nx ** dim
     shape_node = (nx,) * dim
@@ -133,31 +142,34 @@ def make_batch(cfg: Config, n_ops: int | None = None, start: int = 0) -> Operato
         s = [nx] * dim
         s[dim - 1 - ax] = nx + 1                        # C order: axis x is last
         face_shapes.append(tuple(s))
-    faces = [np.empty((N,) + fs) for fs in face_shapes]
-    c = np.zeros((N, n))
+    nf = 0 if params_only else N
+    faces = [np.empty((nf,) + fs) for fs in face_shapes]
+    c = np.zeros((nf, n))
     params = np.empty((N, cfg.fields, n))
-    for j in range(N):
-        i = start + j
+    for j, i in enumerate(indices):
         if cfg.family == "lapv":
             g_node, _ = make_fields(cfg, i, 0)
             v = cfg.vscale * np.exp(g_node)
-            for ax in range(dim):
-                faces[ax][j] = 1.0
-            c[j] = v.reshape(n)
             params[j, 0] = v.reshape(n)
+            if not params_only:
+                for ax in range(dim):
+                    faces[ax][j] = 1.0
+                c[j] = v.reshape(n)
         elif cfg.family == "diva":
             g_node, g_face = make_fields(cfg, i, 0)
-            for ax in range(dim):
-                faces[ax][j] = cfg.vscale * np.exp(g_face[ax])
             params[j, 0] = (cfg.vscale * np.exp(g_node)).reshape(n)
+            if not params_only:
+                for ax in range(dim):
+                    faces[ax][j] = cfg.vscale * np.exp(g_face[ax])
         elif cfg.family == "divac":
             ga_node, ga_face = make_fields(cfg, i, 0)
             gc_node, _ = make_fields(cfg, i, 1)
-            for ax in range(dim):
-                faces[ax][j] = np.exp(ga_face[ax])
-            c[j] = np.exp(gc_node).reshape(n)
             params[j, 0] = np.exp(ga_node).reshape(n)
-            params[j, 1] = c[j]
+            params[j, 1] = np.exp(gc_node).reshape(n)
+            if not params_only:
+                for ax in range(dim):
+                    faces[ax][j] = np.exp(ga_face[ax])
+                c[j] = params[j, 1]
         else:
             raise ValueError(cfg.family)
     assert all(f.shape[1:] == fs for f, fs in zip(faces, face_shapes))

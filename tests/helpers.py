@@ -1,0 +1,38 @@
+"""Shared test helpers: device upload of synth inputs, oracle comparisons."""
+import numpy as np
+
+import synth
+from oracle import checks, eig as oeig, operator as oop
+
+
+def device_problem(fields, device="cuda"):
+    import torch
+    from paper_2510_23215_b200 import scsf
+    faces = [torch.from_numpy(np.ascontiguousarray(f)).to(device) for f in fields.faces]
+    c = torch.from_numpy(np.ascontiguousarray(fields.c)).to(device)
+    params = torch.from_numpy(np.ascontiguousarray(fields.params)).to(device)
+    ops = scsf.assemble(fields.dim, fields.nx, fields.h, faces, c)
+    return ops, params
+
+
+def check_pairs(fields, i, lam_gpu, V_gpu, L, ref=None, guard=8, ev_tol=1e-9, sine_tol=1e-6,
+                resid_tol=1e-8, orth_tol=1e-12, paper_tol=None):
+    """Compare L GPU pairs of operator i with the oracle; returns a dict of measured errors."""
+    A = oop.assemble_csr(fields, i)
+    normA = float(np.abs(A).sum(axis=1).max())
+    if ref is None:
+        ref = oeig.smallest_eigpairs(fields, i, L + guard)
+    lam = np.asarray(lam_gpu[:L])
+    V = np.asarray(V_gpu[:, :L])
+    ev, sine = checks.compare_pairs(ref.lam, ref.V, lam, V, L)
+    r_normA = checks.resid_over_normA(A, lam, V, normA).max()
+    r_paper = checks.rel_residual(A, lam, V).max()
+    orth = checks.orth_error(V)
+    out = dict(ev=ev, sine=sine, r_normA=r_normA, r_paper=r_paper, orth=orth)
+    assert ev <= ev_tol, out
+    assert sine <= sine_tol, out
+    assert r_normA <= resid_tol, out
+    assert orth <= orth_tol, out
+    if paper_tol is not None:
+        assert r_paper <= paper_tol, out
+    return out

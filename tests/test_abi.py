@@ -1,0 +1,74 @@
+"""The C-ABI library loads and exports every symbol include/scsf.h declares — CPU only.
+
+No compute call is made (there is no GPU here); the library is built by
+`paper_2510_23215_b200.build` (nvcc cross-compiles sm_100a without a GPU).
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "scsf.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(scsf_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2510_23215_b200 import build
+    return build.build()
+
+
+def test_header_declares_boundary():
+    names = _declared()
+    for required in ("scsf_sort", "scsf_solve_one", "scsf_solve_queue"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    for name in _declared():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (scsf_\w+)", out))
+    assert set(_declared()) <= exported
+
+
+def test_abi_version_and_binding_table(libpath):
+    from paper_2510_23215_b200 import scsf
+    lib = scsf.load_library(libpath)
+    assert lib.scsf_abi_version() == 1
+    assert sorted(scsf.EXPORTED) == _declared()
+    assert lib.scsf_launch_count() >= 0
+
+
+def test_query_functions_without_gpu(libpath):
+    from paper_2510_23215_b200 import scsf
+    lib = scsf.load_library(libpath)
+    assert lib.scsf_sort_workspace_bytes(1000, 2, 100, 1, 20) > 1000 * 1000 * 8
+    ops = scsf.scsf_ops(2, 100, 100, 1, 1000, 0, 10016, 0)
+    ws = lib.scsf_solve_workspace_bytes(ctypes.byref(ops), 100, 20)
+    assert ws >= 4 * 120 * 10016 * 8
+    assert lib.scsf_sort_workspace_bytes(0, 2, 100, 1, 20) == 0
+
+
+def test_sass_uses_fp64_tensor_cores(libpath):
+    out = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
+    assert "DMMA" in out
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", libpath], capture_output=True, text=True).stdout
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2510_23215_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), fn

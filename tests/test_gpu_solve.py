@@ -1,0 +1,227 @@
+"""Parity of scsf_assemble / scsf_cheb_filter / scsf_solve_* against the oracle — GPU.
+
+Acceptance (BASELINE.json north_star): eigenvalues within 1e-9 relative,
+||Ax - lx|| / ||A||_inf <= 1e-8 per pair, subspace sines <= 1e-6 (per
+cluster, R21), orthonormality 1e-12; the paper metric
+||Ax - lx|| / ||Ax|| is checked against tol with a 10x rounding margin.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import checks, eig as oeig, filter as ofilt, operator as oop
+from oracle import sort as osort
+from tests.helpers import check_pairs, device_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_23215_b200 import scsf
+    scsf.load_library()
+    return scsf
+
+
+def _np_block(t, n):
+    """device block [k, ld] -> numpy n x k (column-major view)."""
+    return t[:, :n].cpu().numpy().T
+
+
+# ------------------------------------------------------------------ assembly ----
+@pytest.mark.parametrize("cfg_name,nx", [("C1", 32), ("C2", 17), ("C3", 23), ("C4", 9), ("C5", 31)])
+def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
+    cfg = synth.get_config(cfg_name).with_(nx=nx)
+    f = synth.make_batch(cfg, 3)
+    ops, _ = device_problem(f)
+    coef = ops.coef.cpu().numpy()
+    for i in range(3):
+        diag, offs = oop.stencil(f, i)
+        n = f.n
+        assert np.allclose(coef[i, 0, :n], diag, rtol=2e-16, atol=0)
+        for d, off in enumerate(offs):
+            assert np.allclose(coef[i, 1 + d, :n], off, rtol=2e-16, atol=0)
+        assert np.all(coef[i, :, n:] == 0.0)
+
+
+# -------------------------------------------------------------------- filter ----
+@pytest.mark.parametrize("cfg_name,nx,k,m", [("C1", 32, 20, 20), ("C3", 29, 9, 7), ("C4", 11, 13, 20),
+                                             ("C2", 40, 1, 1)])
+def test_filter_matches_oracle(lib, cfg_name, nx, k, m):
+    import torch
+    cfg = synth.get_config(cfg_name).with_(nx=nx)
+    f = synth.make_batch(cfg, 2)
+    ops, _ = device_problem(f)
+    n, ld = f.n, ops.ld
+    rng = np.random.default_rng(5)
+    Y0 = rng.standard_normal((n, k))
+    A = oop.assemble_csr(f, 1)
+    normA = float(np.abs(A).sum(axis=1).max())
+    lam, alpha = 0.002 * normA, 0.1 * normA
+    c, e = (alpha + normA) / 2, (normA - alpha) / 2
+    Yd = torch.zeros((k, ld), dtype=torch.float64, device="cuda")
+    Yd[:, :n] = torch.from_numpy(Y0.T.copy())
+    Ym = _np_block(lib.cheb_filter(ops, 1, Yd, m, lam, c, e), n)
+    ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
+    scale = np.abs(ref).max(axis=0)
+    assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * scale)
+
+
+def test_filter_closed_form_laplacian(lib):
+    import torch
+    nx = 24
+    f = synth.constant_fields(2, nx)
+    ops, _ = device_problem(f)
+    h = f.h
+    x = np.arange(1, nx + 1) * h
+    modes = [(1, 1), (1, 2), (5, 3), (24, 24)]
+    V = np.stack([np.outer(np.sin(j * np.pi * x), np.sin(i * np.pi * x)).reshape(-1) for i, j in modes], 1)
+    t = np.array([4 / h ** 2 * (np.sin(i * np.pi * h / 2) ** 2 + np.sin(j * np.pi * h / 2) ** 2) for i, j in modes])
+    beta = 8 / h ** 2
+    alpha = 2000.0
+    c, e = (alpha + beta) / 2, (beta - alpha) / 2
+    Yd = torch.zeros((4, ops.ld), dtype=torch.float64, device="cuda")
+    Yd[:, :f.n] = torch.from_numpy(V.T.copy())
+    Y = _np_block(lib.cheb_filter(ops, 0, Yd, 20, t[0], c, e), f.n)
+    rho = ofilt.cheb_T(20, (t - c) / e) / ofilt.cheb_T(20, np.array([(t[0] - c) / e]))[0]
+    assert np.allclose(Y, V * rho, rtol=0, atol=1e-12 * np.abs(V).max())
+
+
+# --------------------------------------------------------------------- solve ----
+def test_closed_form_laplacian_solve(lib):
+    # O4: constant coefficients; the L cut splits a degenerate pair, so eigenvalues only
+    nx, L, nex = 32, 16, 4
+    f = synth.constant_fields(2, nx, c=1.5)
+    ops, _ = device_problem(f)
+    evals, evecs, st = lib.solve_one(ops, 0, L, nex, 20, 1e-8, 200, seed=1)
+    ex = checks.laplacian_eigs(2, nx, L) + 1.5
+    assert np.abs(evals.cpu().numpy()[:L] - ex).max() <= 1e-9 * ex
+    V = _np_block(evecs, f.n)
+    assert checks.orth_error(V[:, :L]) <= 1e-12
+    A = oop.assemble_csr(f, 0)
+    assert checks.rel_residual(A, evals.cpu().numpy()[:L], V[:, :L]).max() <= 1e-8 * 10
+
+
+def test_c1_full_chain_parity(lib):
+    """configs[0] at full size: all 64 operators along the sorted queue, every one vs the oracle."""
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg)
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    evals, evecs, stats = lib.solve_queue(ops, perm, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=7)
+    ev = evals.cpu().numpy()
+    vecs = evecs.cpu().numpy()
+    for k, i in enumerate(perm):
+        assert stats[k]["status"] == 0, stats[k]
+        check_pairs(f, int(i), ev[k], vecs[k, :, :f.n].T, cfg.L, paper_tol=10 * cfg.tol)
+    assert all(s["warm"] == (k > 0) for k, s in enumerate(stats))
+
+
+@pytest.mark.parametrize("cfg_name,count", [("C2", 5), ("C3", 2), ("C4", 2)])
+def test_full_size_chain_sample(lib, cfg_name, count):
+    """Full-size operators from the head of the sorted queue, solved as one warm chain."""
+    cfg = synth.get_config(cfg_name)
+    f = synth.make_batch(cfg, 24)
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    chain = perm[:count]
+    evals, evecs, stats = lib.solve_queue(ops, chain, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=3)
+    ev = evals.cpu().numpy()
+    for k, i in enumerate(chain):
+        assert stats[k]["status"] == 0, stats[k]
+        V = evecs[k, :, :f.n].cpu().numpy().T
+        check_pairs(f, int(i), ev[k], V, cfg.L, paper_tol=10 * cfg.tol)
+
+
+def test_c5_full_size_properties(lib):
+    """configs[4] (b = 360, global-memory small kernels): residual, orthonormality, Loewner bounds."""
+    cfg = synth.get_config("C5")
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    evals, evecs, st = lib.solve_one(ops, 0, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=5)
+    lam = evals.cpu().numpy()[:cfg.L]
+    V = _np_block(evecs, f.n)[:, :cfg.L]
+    A = oop.assemble_csr(f, 0)
+    normA = float(np.abs(A).sum(axis=1).max())
+    assert checks.resid_over_normA(A, lam, V, normA).max() <= 1e-8
+    assert checks.rel_residual(A, lam, V).max() <= 10 * cfg.tol
+    assert checks.orth_error(V) <= 1e-12
+    lo, hi = checks.loewner_bounds(f, 0, cfg.L)
+    assert np.all(lo <= lam * (1 + 1e-12)) and np.all(lam <= hi * (1 + 1e-12))
+    assert np.all(np.diff(lam) >= 0)
+
+
+# ----------------------------------------------------------------- edge cases ----
+def test_exact_warm_start_converges_without_filtering(lib):
+    # warm start from the exact eigenvectors of the same operator locks at once
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    ev, vecs, st = lib.solve_one(ops, 0, cfg.L, cfg.nex, 20, 1e-8, 200, seed=2)
+    ev2, vecs2, st2 = lib.solve_one(ops, 0, cfg.L, cfg.nex, 20, 1e-8, 200, warm=vecs, seed=2)
+    assert st2["iterations"] <= 1
+    assert np.abs(ev2.cpu().numpy()[:cfg.L] - ev.cpu().numpy()[:cfg.L]).max() <= 1e-12 * ev.cpu().numpy()[cfg.L - 1]
+
+
+def test_identical_operators_chain(lib):
+    # N = 2 identical problems -> the second solve needs (almost) no iteration
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 1)
+    f2 = f.subset([0, 0])
+    ops, _ = device_problem(f2)
+    evals, evecs, stats = lib.solve_queue(ops, [0, 1], cfg.L, cfg.nex, 20, 1e-8, 200, seed=4)
+    assert stats[1]["iterations"] <= 1 < stats[0]["iterations"]
+
+
+def test_tiny_full_block_and_odd_sizes(lib):
+    # b = n (whole spectrum), odd b, L = 1, nex = 0, degree 1
+    f = synth.make_batch(synth.get_config("C1").with_(nx=5), 1)
+    ops, _ = device_problem(f)
+    D = oop.assemble_dense(f, 0)
+    w = np.linalg.eigvalsh(D)
+    for L, nex, m in [(25, 0, 8), (7, 2, 1), (1, 0, 20), (1, 3, 5)]:
+        ev, vecs, st = lib.solve_one(ops, 0, L, nex, m, 1e-10, 500, seed=9)
+        assert np.abs(ev.cpu().numpy()[:L] - w[:L]).max() <= 1e-9 * w[:L].max(), (L, nex, m)
+
+
+def test_max_iter_zero_reports_not_converged(lib):
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    with pytest.raises(lib.NotConverged):
+        lib.solve_one(ops, 0, cfg.L, cfg.nex, 20, 1e-8, 0, seed=1)
+    ev, vecs, st = lib.solve_one(ops, 0, cfg.L, cfg.nex, 20, 1e-8, 0, seed=1, raise_on_fail=False)
+    assert st["status"] == lib.SCSF_ERR_NUMERICAL and st["max_rel_resid"] > 1e-8
+
+
+def test_bad_arguments(lib):
+    import torch
+    f = synth.make_batch(synth.get_config("C1").with_(nx=6), 1)
+    ops, _ = device_problem(f)
+    for L, nex, m, tol in [(0, 1, 20, 1e-8), (30, 10, 20, 1e-8), (4, 1, 0, 1e-8), (4, 1, 20, 0.0)]:
+        with pytest.raises(lib.ScsfError) as ei:
+            lib.solve_one(ops, 0, L, nex, m, tol, 10)
+        assert ei.value.code == lib.SCSF_ERR_ARG
+    with pytest.raises(lib.ScsfError) as ei:
+        lib.solve_one(ops, 0, 4, 1, 20, 1e-8, 10, ws=torch.empty(1024, dtype=torch.uint8, device="cuda"))
+    assert ei.value.code == lib.SCSF_ERR_WORKSPACE
+    with pytest.raises(lib.ScsfError):
+        lib.solve_queue(ops, [0, 3], 4, 1)
+
+
+def test_empty_chain(lib):
+    f = synth.make_batch(synth.get_config("C1").with_(nx=6), 1)
+    ops, _ = device_problem(f)
+    evals, evecs, stats = lib.solve_queue(ops, [], 4, 1)
+    assert evals.shape[0] == 0 and stats == []
+
+
+def test_launch_count_increases(lib):
+    f = synth.make_batch(synth.get_config("C1").with_(nx=6), 1)
+    ops, _ = device_problem(f)
+    before = lib.launch_count()
+    lib.solve_one(ops, 0, 4, 1, 8, 1e-8, 100)
+    assert lib.launch_count() > before
