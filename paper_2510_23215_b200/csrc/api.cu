@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 
 namespace scsf {
@@ -19,6 +20,14 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 void count_launch(int n) { g_launches += n; }
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 // k_sort.cu
 size_t sort_ws_bytes(int N, int dim, int p, int F, int p0);

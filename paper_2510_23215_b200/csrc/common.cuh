@@ -12,6 +12,7 @@ namespace scsf {
 // ---------------------------------------------------------------- errors ----
 void set_error(const char* fmt, ...);
 void count_launch(int n = 1);
+bool debug_sync();   // SCSF_DEBUG_SYNC=1: synchronise and check after every launch
 
 struct Status {
   int code = SCSF_OK;
@@ -31,6 +32,7 @@ struct Status {
   do {                                                                          \
     ::scsf::count_launch();                                                     \
     cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ == cudaSuccess && ::scsf::debug_sync()) e_ = cudaDeviceSynchronize(); \
     if (e_ != cudaSuccess) {                                                    \
       ::scsf::set_error("%s:%d launch: %s", __FILE__, __LINE__,                 \
                         cudaGetErrorString(e_));                                \

@@ -171,8 +171,12 @@ int tn_splits(int64_t n, int b1, int b2) {
   return min(want, maxs);
 }
 
+// Upper bound of splits * b1' * b2' over every call with b1' <= b1, b2' <= b2:
+// splits <= ceil(296 / tiles) and tiles >= b1' b2' / 64^2, so
+// splits * b1' * b2' <= 296 * 64^2 + b1' * b2'.
 size_t tn_partial_doubles(int64_t n, int b1, int b2) {
-  return (size_t)tn_splits(n, b1, b2) * b1 * b2;
+  (void)n;
+  return (size_t)2 * 148 * TN_BM * TN_BM + (size_t)b1 * b2;
 }
 
 // C (b1 x b2, ldc) = alpha X^T Y.  P: workspace of tn_partial_doubles.
