@@ -190,6 +190,53 @@ int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
                      double* evals, double* evecs, int64_t ld_vec, scsf_stats* st,
                      void* ws, size_t ws_bytes, void* stream);
 
+/*
+ * Several warm-start chains of one queue solved concurrently on one GPU — the
+ * paper's "N problems partitioned into M independent chunks, M instances of
+ * SCSF in parallel" with a chunk per chain.  Chain c is
+ * queue[chain_start[c] .. chain_start[c+1]) (contiguous slices of the sorted
+ * order); each runs on its own host thread and CUDA stream with its own
+ * workspace slice, so latency-bound kernels of different chains overlap.
+ *  queue        host [chain_start[n_chains]]: operator indices
+ *  chain_start  host [n_chains + 1], chain_start[0] = 0, non-decreasing
+ *  evals / evecs / st  indexed by queue position (as scsf_solve_queue)
+ *  ws_bytes     >= n_chains * scsf_solve_workspace_bytes(ops, L, nex)
+ * The caller's stream is synchronised before the chains start; the call
+ * returns when every chain has finished.  Return value: worst status.
+ */
+int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                      int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol,
+                      int32_t max_iter, uint64_t seed, double* evals, double* evecs, int64_t ld_vec,
+                      scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------- component entry points ---- */
+/*
+ * Single steps of Alg. 3 exposed for parity tests and microbenchmarks.  Same
+ * conventions as above; all pointers device; synchronous; ws from the query.
+ *
+ * scsf_gemm_tn:  C (b1 x b2, ldc) = alpha X^T Y, X n x b1 (ldx), Y n x b2 (ldy):
+ *   the Gram / Rayleigh-quotient contraction (Alg. 3 ll. 4-5).
+ *   upper != 0: only the upper triangle (i <= j, b1 == b2) is defined on return.
+ * scsf_gemm_nn:  Out (n x b2, ldo) = alpha X M + beta Out, X n x b1, M b1 x b2
+ *   (ldm): the basis rotation / triangular apply (ll. 4 and 6).
+ *   Out may alias X (in-place) when ldo == ldx.
+ * scsf_chol_inv: S (b x b, upper triangle used) = R^T R; writes R^{-1} (b x b,
+ *   upper, ld b): CholQR's small factor (l. 4, reading R13).  Returns
+ *   SCSF_ERR_NUMERICAL if S needed the shifted fallback.
+ * scsf_syev_small: G (b x b, upper triangle used) = Z diag(theta) Z^T, theta
+ *   ascending (b), Z (b x b, ld b): the reduced eigenproblem (l. 6).
+ */
+size_t scsf_dev_workspace_bytes(int64_t n, int32_t b1, int32_t b2);
+int scsf_gemm_tn(const double* X, int64_t ldx, int32_t b1, const double* Y, int64_t ldy, int32_t b2,
+                 int64_t n, double alpha, int32_t upper, double* C, int64_t ldc, void* ws,
+                 size_t ws_bytes, void* stream);
+int scsf_gemm_nn(const double* X, int64_t ldx, int64_t n, int32_t b1, const double* M, int64_t ldm,
+                 int32_t b2, double alpha, double beta, double* Out, int64_t ldo, void* stream);
+int scsf_chol_inv(const double* S, int64_t lds, int32_t b, int64_t nrows, double* Rinv, void* ws,
+                  size_t ws_bytes, void* stream);
+int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z, void* ws,
+                    size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------- helpers ---- */
 
 const char* scsf_last_error(void);   /* thread-local message for the last non-OK status */

@@ -7,6 +7,9 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
 
 namespace scsf {
 
@@ -35,8 +38,26 @@ int signatures_impl(const double* params, int N, int dim, int p, int F, int p0, 
                     cudaStream_t s);
 int sort_impl(const double* params, int N, int dim, int p, int F, int p0, int start, int* perm,
               double* d2_best, double* d2_second, Arena& a, cudaStream_t s);
+// k_dense.cu / k_small.cu primitives
+size_t tn_partial_doubles(int64_t n, int b1, int b2);
+int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, int b2, int64_t n,
+            double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s);
+int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+            double alpha, double beta, double* Out, int64_t ldo, cudaStream_t s);
+int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
+                  Ctrl* ctrl, cudaStream_t s);
+int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
+                double* Zout, Ctrl* ctrl, cudaStream_t s);
 // solver.cu
 int set_timing(int on);
+// k_small.cu / k_dense.cu: one-time kernel attributes (set before any worker thread starts)
+int set_small_attrs();
+int dense_init_attrs();
+static int init_kernel_attrs() {
+  SCSF_TRY(set_small_attrs());
+  SCSF_TRY(dense_init_attrs());
+  return SCSF_OK;
+}
 // k_stencil.cu
 int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
                   const double* c, double* coef, cudaStream_t s);
@@ -221,26 +242,17 @@ int scsf_solve_one(const scsf_ops* ops, int32_t op_index, int32_t L, int32_t nex
   return r;
 }
 
-int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
+// One warm-start chain on one stream: chain[0] cold, every later operator warm
+// from the previous final block.  Outputs by chain position.
+static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
                      int32_t degree, double tol, int32_t max_iter, uint64_t seed, double* evals, double* evecs,
-                     int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes, void* stream) {
-  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
-  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
-  SCSF_ARG_CHECK(n_chain >= 0, "n_chain must be >= 0");
-  SCSF_ARG_CHECK(n_chain == 0 || chain != nullptr, "chain is NULL");
-  SCSF_ARG_CHECK(n_chain == 0 || evals != nullptr, "evals is NULL");
-  SCSF_ARG_CHECK(evecs == nullptr || ld_vec >= n, "ld_vec must be >= n");
-  for (int k = 0; k < n_chain; ++k)
-    SCSF_ARG_CHECK(chain[k] >= 0 && chain[k] < ops->n_ops, "chain[%d]=%d out of range", k, chain[k]);
-  if (n_chain == 0) return SCSF_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  SolveWS w;
-  SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w));
+                     int64_t ld_vec, scsf_stats* st, SolveWS& w, cudaStream_t s) {
+  const int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
   int worst = SCSF_OK;
   for (int k = 0; k < n_chain; ++k) {
     scsf_stats local{};
-    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0, false, seed + (uint64_t)chain[k],
-                       w, &local, s);
+    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0, false, seed + (uint64_t)chain[k], w,
+                       &local, s);
     if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
     if (r > worst) worst = r;
     if (st) st[k] = local;
@@ -253,6 +265,176 @@ int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   }
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
   return worst;
+}
+
+static int check_queue(const scsf_ops* ops, const int32_t* queue, int32_t len, double* evals, double* evecs,
+                       int64_t ld_vec) {
+  int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  SCSF_ARG_CHECK(len >= 0, "chain length must be >= 0");
+  SCSF_ARG_CHECK(len == 0 || queue != nullptr, "chain is NULL");
+  SCSF_ARG_CHECK(len == 0 || evals != nullptr, "evals is NULL");
+  SCSF_ARG_CHECK(evecs == nullptr || ld_vec >= n, "ld_vec must be >= n");
+  for (int k = 0; k < len; ++k)
+    SCSF_ARG_CHECK(queue[k] >= 0 && queue[k] < ops->n_ops, "chain[%d]=%d out of range", k, queue[k]);
+  return SCSF_OK;
+}
+
+int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
+                     int32_t degree, double tol, int32_t max_iter, uint64_t seed, double* evals, double* evecs,
+                     int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
+  SCSF_TRY(check_queue(ops, chain, n_chain, evals, evecs, ld_vec));
+  if (n_chain == 0) return SCSF_OK;
+  SCSF_TRY(init_kernel_attrs());
+  SolveWS w;
+  SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w));
+  return run_chain(ops, chain, n_chain, L, nex, degree, tol, max_iter, seed, evals, evecs, ld_vec, st, w,
+                   (cudaStream_t)stream);
+}
+
+int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start, int32_t n_chains,
+                      int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter, uint64_t seed,
+                      double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes,
+                      void* stream) {
+  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
+  SCSF_ARG_CHECK(n_chains >= 1 && chain_start != nullptr, "n_chains >= 1 and chain_start required");
+  SCSF_ARG_CHECK(chain_start[0] == 0, "chain_start[0] must be 0");
+  for (int c = 0; c < n_chains; ++c)
+    SCSF_ARG_CHECK(chain_start[c + 1] >= chain_start[c], "chain_start must be non-decreasing");
+  const int32_t len = chain_start[n_chains];
+  SCSF_TRY(check_queue(ops, queue, len, evals, evecs, ld_vec));
+  if (len == 0) return SCSF_OK;
+  const size_t per = solve_ws_bytes(ops, L, nex);
+  if (!ws || ws_bytes < per * (size_t)n_chains) {
+    set_error("workspace too small: need %zu bytes (%d chains), got %zu", per * (size_t)n_chains, n_chains,
+              ws_bytes);
+    return SCSF_ERR_WORKSPACE;
+  }
+  cudaStream_t caller = (cudaStream_t)stream;
+  SCSF_TRY(init_kernel_attrs());
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(caller));   // inputs produced on the caller's stream are ready
+  int dev = 0;
+  SCSF_CUDA_CHECK(cudaGetDevice(&dev));
+  std::vector<int> status(n_chains, SCSF_OK);
+  std::vector<std::string> msg(n_chains);
+  auto worker = [&](int c) {
+    cudaSetDevice(dev);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      status[c] = SCSF_ERR_DEVICE;
+      msg[c] = "cudaStreamCreate failed";
+      return;
+    }
+    SolveWS w;
+    int r = carve_solve_ws(ops, L, nex, (char*)ws + per * (size_t)c, per, w);
+    const int32_t b0 = chain_start[c], cnt = chain_start[c + 1] - chain_start[c];
+    if (r == SCSF_OK && cnt > 0)
+      r = run_chain(ops, queue + b0, cnt, L, nex, degree, tol, max_iter, seed, evals + (int64_t)b0 * L,
+                    evecs ? evecs + (int64_t)b0 * L * ld_vec : nullptr, ld_vec, st ? st + b0 : nullptr, w, s);
+    status[c] = r;
+    if (r != SCSF_OK) msg[c] = scsf_last_error();
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  };
+  std::vector<std::thread> th;
+  th.reserve(n_chains);
+  for (int c = 0; c < n_chains; ++c) th.emplace_back(worker, c);
+  for (auto& t : th) t.join();
+  int worst = SCSF_OK;
+  for (int c = 0; c < n_chains; ++c) {
+    const int r = status[c];
+    if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) {
+      set_error("chain %d: %s", c, msg[c].c_str());
+      return r;
+    }
+    if (r > worst) {
+      worst = r;
+      set_error("chain %d: %s", c, msg[c].c_str());
+    }
+  }
+  return worst;
+}
+
+size_t scsf_dev_workspace_bytes(int64_t n, int32_t b1, int32_t b2) {
+  Arena a(nullptr, 0);
+  const int bm = b1 > b2 ? b1 : b2;
+  a.take<double>((int64_t)tn_partial_doubles(n, b1, b2));
+  a.take<double>(3 * (int64_t)bm * bm + 2);
+  a.take<Ctrl>(1);
+  return a.off;
+}
+
+int scsf_gemm_tn(const double* X, int64_t ldx, int32_t b1, const double* Y, int64_t ldy, int32_t b2, int64_t n,
+                 double alpha, int32_t upper, double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_ARG_CHECK(X && Y && C && b1 >= 1 && b2 >= 1 && n >= 1, "bad gemm_tn arguments");
+  SCSF_ARG_CHECK(ldx >= n && ldy >= n && ldc >= b1, "bad leading dimensions");
+  SCSF_ARG_CHECK(!upper || b1 == b2, "upper requires b1 == b2");
+  Arena a(ws, ws_bytes);
+  double* P = a.take<double>((int64_t)tn_partial_doubles(n, b1, b2));
+  if (a.overflow || !ws) {
+    set_error("workspace too small");
+    return SCSF_ERR_WORKSPACE;
+  }
+  SCSF_TRY(init_kernel_attrs());
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_TRY(gemm_tn(X, ldx, b1, Y, ldy, b2, n, alpha, upper, C, ldc, P, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+int scsf_gemm_nn(const double* X, int64_t ldx, int64_t n, int32_t b1, const double* M, int64_t ldm, int32_t b2,
+                 double alpha, double beta, double* Out, int64_t ldo, void* stream) {
+  SCSF_ARG_CHECK(X && M && Out && b1 >= 1 && b2 >= 1 && n >= 1, "bad gemm_nn arguments");
+  SCSF_ARG_CHECK(ldx >= n && ldo >= n && ldm >= b1, "bad leading dimensions");
+  SCSF_ARG_CHECK(Out != X || ldo == ldx, "in-place needs ldo == ldx");
+  SCSF_TRY(init_kernel_attrs());
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_TRY(gemm_nn(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+int scsf_chol_inv(const double* S, int64_t lds, int32_t b, int64_t nrows, double* Rinv, void* ws, size_t ws_bytes,
+                  void* stream) {
+  SCSF_ARG_CHECK(S && Rinv && b >= 1 && b <= 384 && lds >= b, "bad chol_inv arguments");
+  Arena a(ws, ws_bytes);
+  double* scratch = a.take<double>((int64_t)b * b);
+  Ctrl* ctrl = a.take<Ctrl>(1);
+  if (a.overflow || !ws) {
+    set_error("workspace too small");
+    return SCSF_ERR_WORKSPACE;
+  }
+  SCSF_TRY(init_kernel_attrs());
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_CUDA_CHECK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
+  SCSF_TRY(chol_inv_impl(S, lds, b, nrows, Rinv, scratch, ctrl, s));
+  Ctrl h{};
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (h.chol_fail) {
+    set_error("Gram matrix not numerically SPD: shifted factor returned");
+    return SCSF_ERR_NUMERICAL;
+  }
+  return SCSF_OK;
+}
+
+int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z, void* ws, size_t ws_bytes,
+                    void* stream) {
+  SCSF_ARG_CHECK(G && theta && Z && b >= 1 && b <= 384 && ldg >= b, "bad syev_small arguments");
+  Arena a(ws, ws_bytes);
+  double* g = a.take<double>((int64_t)b * b + 2);
+  double* zw = a.take<double>((int64_t)b * b);
+  Ctrl* ctrl = a.take<Ctrl>(1);
+  if (a.overflow || !ws) {
+    set_error("workspace too small");
+    return SCSF_ERR_WORKSPACE;
+  }
+  SCSF_TRY(init_kernel_attrs());
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_CUDA_CHECK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
+  SCSF_TRY(jacobi_impl(G, ldg, b, g, zw, theta, Z, ctrl, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
 }
 
 }  // extern "C"

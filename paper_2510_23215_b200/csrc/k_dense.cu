@@ -84,21 +84,18 @@ __global__ void __launch_bounds__(128) k_gemm_tn(const double* __restrict__ X, i
       }
 }
 
-// C[i + j ldc] = alpha * sum_z P[z][i + j b1]  (z ascending); sym: average with the transpose.
+// C[i + j ldc] = alpha * sum_z P[z][i + j b1]  (z ascending, fixed order: deterministic).
+// Symmetric results (Gram, Rayleigh quotient) are symmetrised by their consumers on load.
 __global__ void k_reduce_partials(const double* __restrict__ P, int splits, int b1, int b2,
-                                  double alpha, int sym, double* __restrict__ C, int64_t ldc) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)b1 * b2) return;
-  int i = (int)(idx % b1), j = (int)(idx / b1);
+                                  double alpha, double* __restrict__ C, int64_t ldc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= b1) return;
   const int64_t stride = (int64_t)b1 * b2;
+  const double* p = P + i + (int64_t)j * b1;
   double s = 0.0;
-  for (int z = 0; z < splits; ++z) s += P[z * stride + idx];
-  if (sym) {
-    double s2 = 0.0;
-    int64_t tidx = j + (int64_t)i * b1;
-    for (int z = 0; z < splits; ++z) s2 += P[z * stride + tidx];
-    s = 0.5 * (s + s2);
-  }
+#pragma unroll 8
+  for (int z = 0; z < splits; ++z) s += __ldg(p + z * stride);
   C[i + (int64_t)j * ldc] = alpha * s;
 }
 
@@ -161,13 +158,238 @@ __global__ void __launch_bounds__(128) k_gemm_nn(const double* __restrict__ X, i
   }
 }
 
+// =====================================================================
+// v2 tiles: 256 threads (8 warps, 2 x 4), 64 x 64 CTA tile, warp tile 32 x 16
+// (4 x 2 DMMA m8n8k4 per k-step), k-chunks of 32 moved by cp.async into a
+// 2-stage shared-memory ring.  Shared-memory row pitch 36 doubles (= 4 mod 16)
+// makes every fragment load conflict-free per half-warp.
+// =====================================================================
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int V2_T = 64, V2_KC = 32, V2_P = V2_KC + 4;   // tile, k-chunk, pitch
+
+// ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
+__global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
+                                                  const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
+                                                  int64_t kchunk, int upper, double* __restrict__ P) {
+  extern __shared__ __align__(16) double smd[];
+  double* xs = smd;                                  // [2][64][36]
+  double* ys = smd + 2 * V2_T * V2_P;                // [2][64][36]
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  if (upper && ti > tj) return;
+  const int i0 = ti * V2_T, j0 = tj * V2_T;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = min(n, kbeg + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int nck = (int)((kend - kbeg + V2_KC - 1) / V2_KC);
+
+  auto issue = [&](int c, int stage) {
+    const int64_t k0 = kbeg + (int64_t)c * V2_KC;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + 256 * q;               // 0..1023
+      const int col = idx >> 4, seg = idx & 15;    // 64 columns x 16 16-byte segments
+      const int64_t k = k0 + 2 * seg;
+      const int rem = (int)max((int64_t)0, min((int64_t)2, kend - k));
+      double* dx = xs + (stage * V2_T + col) * V2_P + 2 * seg;
+      double* dy = ys + (stage * V2_T + col) * V2_P + 2 * seg;
+      const bool okx = (i0 + col < b1) && rem > 0, oky = (j0 + col < b2) && rem > 0;
+      cp_async16(dx, okx ? (const void*)(X + k + (int64_t)(i0 + col) * ldx) : (const void*)X, okx ? 8 * rem : 0);
+      cp_async16(dy, oky ? (const void*)(Y + k + (int64_t)(j0 + col) * ldy) : (const void*)Y, oky ? 8 * rem : 0);
+    }
+  };
+
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  issue(0, 0);
+  cp_commit();
+  for (int c = 0; c < nck; ++c) {
+    if (c + 1 < nck) {
+      issue(c + 1, (c + 1) & 1);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const double* xa = xs + ((c & 1) * V2_T + wm + g) * V2_P + t;
+    const double* yb = ys + ((c & 1) * V2_T + wn + g) * V2_P + t;
+#pragma unroll
+    for (int kk = 0; kk < V2_KC; kk += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * V2_P + kk];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = yb[ni * 8 * V2_P + kk];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+    __syncthreads();
+  }
+  double* out = P + (int64_t)blockIdx.z * b1 * b2;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + 2 * t + e;
+        if (i < b1 && j < b2) out[i + (int64_t)j * b1] = acc[mi][ni][e];
+      }
+}
+
+// ---- NN: Out[r0:r0+64, :] = alpha X[r0:r0+64, 0:b1] M + beta Out.  The whole
+// 64-row panel of X stays resident (so Out may alias X); M streams through a
+// 2-stage ring in k-chunks.  tri_upper: M is upper triangular, chunks with
+// k > last column of the pass are skipped.
+constexpr int NN2_MAX_K = 128;
+
+__global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
+                                                  const double* __restrict__ M, int64_t ldm, int b2,
+                                                  double alpha, double beta, double* Out, int64_t ldo,
+                                                  int tri_upper) {
+  extern __shared__ __align__(16) double smd[];
+  const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
+  double* xp = smd;                                  // [b1r][68]: xp[k*68 + r]
+  double* ms = smd + b1r * (V2_T + 4);               // [2][64][36]: ms[(st*64 + j)*36 + kk]
+  const int64_t r0 = (int64_t)blockIdx.x * V2_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int nck_all = b1r / V2_KC;
+  const int rows_here = (int)min((int64_t)V2_T, n - r0);
+
+  auto issue_panel = [&](int c) {      // 32 k-columns x 64 rows: 32 x 32 16-byte segments
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + 256 * q;
+      const int kk = idx >> 5, seg = idx & 31;
+      const int k = c * V2_KC + kk;
+      const int rr = 2 * seg;
+      const int rem = (k < b1) ? max(0, min(2, rows_here - rr)) : 0;
+      cp_async16(xp + k * (V2_T + 4) + rr, rem ? (const void*)(X + r0 + rr + (int64_t)k * ldx) : (const void*)X,
+                 8 * rem);
+    }
+  };
+  auto issue_m = [&](int c, int j0, int stage) {   // 64 columns x 32 k (8-byte copies; ldm may be odd)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + 256 * q;               // 0..2047
+      const int j = idx >> 5, kk = idx & 31;
+      const int k = c * V2_KC + kk;
+      const bool ok = (k < b1) && (j0 + j < b2);
+      cp_async8(ms + (stage * V2_T + j) * V2_P + kk, ok ? (const void*)(M + k + (int64_t)(j0 + j) * ldm) : (const void*)M,
+                ok ? 8 : 0);
+    }
+  };
+
+  for (int j0 = 0; j0 < b2; j0 += V2_T) {
+    const bool first = (j0 == 0);
+    const int nck = tri_upper ? min(nck_all, (min(b2, j0 + V2_T) + V2_KC - 1) / V2_KC) : nck_all;
+    // the whole panel is needed before any write: in the first pass load every chunk
+    const int ncp = first ? nck_all : 0;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    // groups: G_c = {M chunk c, panel chunk c (first pass)}; remaining panel chunks ride on the last group
+    for (int c = 0; c < 2 && c < nck; ++c) {
+      issue_m(c, j0, c);
+      if (c < ncp) issue_panel(c);
+      cp_commit();
+    }
+    for (int c = 0; c < nck; ++c) {
+      if (c + 1 < nck) cp_wait<1>();
+      else cp_wait<0>();
+      __syncthreads();
+      const double* xa = xp + (c * V2_KC + t) * (V2_T + 4) + wm + g;
+      const double* mb = ms + ((c & 1) * V2_T + wn + g) * V2_P + t;
+#pragma unroll
+      for (int kk = 0; kk < V2_KC; kk += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * (V2_T + 4) + mi * 8];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = mb[ni * 8 * V2_P + kk];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+      }
+      __syncthreads();
+      if (c + 2 < nck) {
+        issue_m(c + 2, j0, c & 1);
+        if (c + 2 < ncp) issue_panel(c + 2);
+        cp_commit();
+      }
+    }
+    if (first && nck < ncp) {        // triangular M cut the first pass short: finish the panel
+      for (int c = nck; c < ncp; ++c) issue_panel(c);
+      cp_commit();
+      cp_wait<0>();
+    }
+    __syncthreads();                 // every warp is past its panel reads before anyone writes Out
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = r0 + wm + mi * 8 + g;
+          const int j = j0 + wn + ni * 8 + 2 * t + e;
+          if (r < n && j < b2) {
+            double* o = Out + r + (int64_t)j * ldo;
+            double v = alpha * acc[mi][ni][e];
+            if (beta != 0.0) v = fma(beta, *o, v);
+            *o = v;
+          }
+        }
+  }
+}
+
 // ------------------------------------------------------------------ host ----
 static int g_nn_smem_set = 0;
+
+static size_t tn2_smem() { return (size_t)4 * V2_T * V2_P * sizeof(double); }
+static size_t nn2_smem(int b1) {
+  const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
+  return ((size_t)b1r * (V2_T + 4) + (size_t)2 * V2_T * V2_P) * sizeof(double);
+}
+
+int dense_init_attrs() {
+  if (g_nn_smem_set) return SCSF_OK;
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       NN_MAX_K * NN_LDS * (int)sizeof(double)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn2_smem()));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn2_smem(NN2_MAX_K)));
+  g_nn_smem_set = 1;
+  return SCSF_OK;
+}
 
 int tn_splits(int64_t n, int b1, int b2) {
   int tiles = ceil_div(b1, TN_BM) * ceil_div(b2, TN_BM);
   int want = max(1, (2 * 148 + tiles - 1) / tiles);
-  int maxs = max(1, ceil_div(n, 4 * TN_KC));        // at least 4 chunks per split
+  int maxs = max(1, ceil_div(n, 128));              // at least 128 rows (4 k-chunks) per split
   return min(want, maxs);
 }
 
@@ -180,38 +402,52 @@ size_t tn_partial_doubles(int64_t n, int b1, int b2) {
 }
 
 // C (b1 x b2, ldc) = alpha X^T Y.  P: workspace of tn_partial_doubles.
+// upper (b1 == b2): only the upper-triangle tiles are computed and reduced;
+// the consumers (Cholesky, Jacobi) read the upper triangle only.
 int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, int b2, int64_t n,
             double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s) {
   if (b1 <= 0 || b2 <= 0) return SCSF_OK;
+  SCSF_TRY(dense_init_attrs());
+  const int upper = (sym && b1 == b2) ? 1 : 0;
   int splits = tn_splits(n, b1, b2);
-  int64_t kchunk = round_up(ceil_div(n, splits), TN_KC);
+  if (upper) {
+    const int t = ceil_div(b1, V2_T);
+    splits = min(max(1, ceil_div(n, 128)), max(1, (2 * 148 + t * (t + 1) / 2 - 1) / (t * (t + 1) / 2)));
+  }
+  int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
   splits = ceil_div(n, kchunk);
-  dim3 g(ceil_div(b1, TN_BM), ceil_div(b2, TN_BM), splits);
-  k_gemm_tn<<<g, 128, 0, s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, P);
+  dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
+  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, P);
   SCSF_LAUNCH_CHECK();
-  k_reduce_partials<<<ceil_div((int64_t)b1 * b2, 256), 256, 0, s>>>(P, splits, b1, b2, alpha, sym, C, ldc);
+  dim3 gr(ceil_div(b1, 128), b2);
+  k_reduce_partials<<<gr, 128, 0, s>>>(P, splits, b1, b2, alpha, C, ldc);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
 
-// Out (n x b2, ldo) = alpha X M + beta Out;  Out may alias X.
-int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
-            double alpha, double beta, double* Out, int64_t ldo, cudaStream_t s) {
+// Out (n x b2, ldo) = alpha X M + beta Out;  Out may alias X.  tri: M upper triangular.
+int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+               double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s) {
   if (b2 <= 0 || n <= 0) return SCSF_OK;
   if (b1 > NN_MAX_K) {
     set_error("gemm_nn: inner dimension %d exceeds %d", b1, NN_MAX_K);
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
-  if (!g_nn_smem_set) {
-    SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         NN_MAX_K * NN_LDS * (int)sizeof(double)));
-    g_nn_smem_set = 1;
+  SCSF_TRY(dense_init_attrs());
+  if (b1 <= NN2_MAX_K) {
+    k_gemm_nn2<<<ceil_div(n, V2_T), 256, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri);
+  } else {
+    int b1r = (max(b1, 1) + 3) & ~3;
+    size_t smem = (size_t)b1r * NN_LDS * sizeof(double);
+    k_gemm_nn<<<ceil_div(n, NN_BM), 128, smem, s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo);
   }
-  int b1r = (max(b1, 1) + 3) & ~3;
-  size_t smem = (size_t)b1r * NN_LDS * sizeof(double);
-  k_gemm_nn<<<ceil_div(n, NN_BM), 128, smem, s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
+}
+
+int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+            double alpha, double beta, double* Out, int64_t ldo, cudaStream_t s) {
+  return gemm_nn_ex(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, 0, s);
 }
 
 }  // namespace scsf

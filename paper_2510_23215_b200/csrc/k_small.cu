@@ -20,57 +20,76 @@
 namespace scsf {
 
 // ------------------------------------------------------------- chol_inv ----
-// Working array A (b x b, col-major, ld b): upper triangle -> R, strict lower
-// triangle -> R^{-1} transposed (X[k][c] stored at A[c + k b], k < c),
-// dinv[i] = 1/R[i][i].
+// Cholesky with the inverse factor built in the same elimination sweep
+// (Gauss-Jordan on [S | I]): at step j, row j of R = A[j, j:] / r_jj and the
+// trailing block is updated; the same row operations applied to I give
+// B = L^{-1} = (R^{-1})^T.  Storage: A (b x b, col-major, ld b): upper triangle
+// holds A / R, strict lower triangle holds B (B[i][c] at A[i + c b], c < i);
+// binv[i] = B[i][i].  1024 threads as 32 x 32 (tx = lane, ty = warp): every
+// loop is a strided 2-D loop, no runtime integer division.
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S, int64_t lds, int b,
                                                    int64_t nrows, double* __restrict__ Rinv,
                                                    double* __restrict__ gA, Ctrl* ctrl) {
   extern __shared__ double sm[];
   double* A = SMEM ? sm : gA;
-  __shared__ double dinv[384];
+  __shared__ double binv[384];
+  __shared__ double rj[384], bj[384];   // row j of R and of B, contiguous (no bank conflicts)
   __shared__ int fail;
   __shared__ double shift;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (tid == 0) {
       fail = 0;
+      shift = 0.0;
       if (attempt == 1) {
         double tr = 0.0;
         for (int i = 0; i < b; ++i) tr += fabs(S[i + i * lds]);
         shift = 11.0 * ((double)nrows * b + (double)b * (b + 1)) * 1.1102230246251565e-16 * tr;
-      } else {
-        shift = 0.0;
       }
     }
     __syncthreads();
-    for (int idx = tid; idx < b * b; idx += nt) {
-      int i = idx % b, j = idx / b;
-      double v = S[i + (int64_t)j * lds];
-      if (i == j) v += shift;
-      A[idx] = v;
-    }
+    // load: symmetrised upper triangle (+ shift on the diagonal), zero lower triangle
+    for (int k = ty; k < b; k += 32)
+      for (int i = tx; i < b; i += 32) {
+        double v = 0.0;
+        if (i < k) v = S[i + k * lds];                 // Gram: upper triangle is the valid half
+        else if (i == k) v = S[i + i * lds] + shift;
+        A[i + k * b] = v;
+      }
+    for (int i = tid; i < b; i += 1024) binv[i] = 1.0;
     __syncthreads();
-    // right-looking upper Cholesky; breakdown when a pivot loses all but ~1e-14 of its diagonal
     for (int j = 0; j < b; ++j) {
-      double d = A[j + j * b];
+      const double d = A[j + j * b];
+      const double bj_old = binv[j];
       if (!(d > 1e-14 * fabs(S[j + (int64_t)j * lds])) || !isfinite(d)) {
         if (tid == 0) fail = 1;
       }
-      __syncthreads();
+      __syncthreads();                       // every thread has read d and bj_old
       if (fail) break;
-      double r = sqrt(d);
-      for (int k = j + 1 + tid; k < b; k += nt) A[j + k * b] /= r;
-      if (tid == 0) A[j + j * b] = r;
+      const double r = sqrt(d), rinv = 1.0 / r;
+      const double bjj = bj_old * rinv;      // B[j][j] after scaling
+      // phase 1: row j of R and row j of B scaled by 1/r_jj (B row kept in A for the output)
+      for (int k = j + 1 + tid; k < b; k += 1024) rj[k] = A[j + k * b] * rinv;
+      for (int c = tid; c < j; c += 1024) {
+        const double v = A[j + c * b] * rinv;
+        bj[c] = v;
+        A[j + c * b] = v;
+      }
+      if (tid == 0) {
+        A[j + j * b] = r;
+        binv[j] = bjj;
+        bj[j] = bjj;
+      }
       __syncthreads();
-      // trailing update of the upper triangle: A[i][k] -= R[j][i] R[j][k], j < i <= k
-      const int m = b - j - 1;
-      for (int t = tid; t < m * m; t += nt) {
-        int ii = t % m, kk = t / m;
-        if (ii > kk) continue;
-        int i = j + 1 + ii, k = j + 1 + kk;
-        A[i + k * b] -= A[j + i * b] * A[j + k * b];
+      // phase 2: trailing update (upper, j < i <= k) and B rows i > j
+      for (int k = j + 1 + ty; k < b; k += 32) {
+        const double rjk = rj[k];
+        for (int i = j + 1 + tx; i <= k; i += 32) A[i + k * b] -= rj[i] * rjk;
+      }
+      for (int c = ty; c <= j; c += 32) {
+        const double bjc = bj[c];
+        for (int i = j + 1 + tx; i < b; i += 32) A[i + c * b] -= rj[i] * bjc;
       }
       __syncthreads();
     }
@@ -81,149 +100,177 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S,
     }
     __syncthreads();
   }
-  // R^{-1}: rows from the bottom; X[i][c] = -(sum_{k=i+1..c} R[i][k] X[k][c]) / R[i][i]
-  for (int i = b - 1; i >= 0; --i) {
-    double rii = A[i + i * b];
-    if (tid == 0) dinv[i] = 1.0 / rii;
-    for (int c = i + 1 + tid; c < b; c += nt) {
-      double s = 0.0;
-      for (int k = i + 1; k <= c; ++k) {
-        double xkc = (k == c) ? (1.0 / A[c + c * b]) : A[c + k * b];   // X[k][c]
-        s = fma(A[i + k * b], xkc, s);
-      }
-      A[c + i * b] = -s / rii;   // X[i][c] stored transposed in the lower triangle
+  // R^{-1}[i][c] = B[c][i] (upper)
+  for (int c = ty; c < b; c += 32)
+    for (int i = tx; i < b; i += 32) {
+      double v = 0.0;
+      if (i == c) v = binv[i];
+      else if (i < c) v = A[c + i * b];
+      Rinv[i + c * b] = v;
     }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < b * b; idx += nt) {
-    int i = idx % b, c = idx / b;
-    double v = 0.0;
-    if (i == c) v = dinv[i];
-    else if (i < c) v = A[c + i * b];
-    Rinv[idx] = v;
-  }
 }
 
 // ----------------------------------------------------------- jacobi_eig ----
-// Parallel-order (round-robin) two-sided Jacobi.  G (b x b, ld b) is copied to
-// the work array; Z accumulates the rotations (global scratch, ld b).
+// Two-sided cyclic Jacobi in parallel round-robin order on a packed symmetric
+// G (upper triangle, gidx) with the rotation accumulator Z (b x b).  Each
+// round rotates b/2 disjoint pairs at once; G's 2x2 blocks (m1 <= m2) and
+// Z's column pairs are updated in place (each element has one owner).  A
+// sweep starts only if some |g_pq| > tol sqrt(|g_pp g_qq|): a warm, nearly
+// diagonal G costs one check.
+__device__ __forceinline__ int gidx(int i, int j) {
+  return (i <= j) ? ((j * (j + 1)) >> 1) + i : ((i * (i + 1)) >> 1) + j;
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Gin, int64_t ldg, int b,
-                                                 double* __restrict__ gG, double* __restrict__ Z,
+                                                 double* __restrict__ gG, double* __restrict__ gZ,
                                                  double* __restrict__ theta_out, double* __restrict__ Zout,
                                                  int max_sweeps, Ctrl* ctrl) {
   extern __shared__ double sm[];
+  const int npk = (b * (b + 1)) >> 1;
   double* G = SMEM ? sm : gG;
+  double* Z = SMEM ? sm + ((npk + 1) & ~1) : gZ;
   __shared__ double cs_c[192], cs_s[192], cs_t[192];
   __shared__ int cs_p[192], cs_q[192], cs_rot[192];
-  __shared__ int any_rot;
+  __shared__ double red[32];
   __shared__ double diag_s[384];
   __shared__ int rank_s[384];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int bp = (b + 1) & ~1;      // even; index b is a dummy when b is odd
-  const int half = bp / 2;
-  for (int idx = tid; idx < b * b; idx += nt) {
-    int i = idx % b, j = idx / b;
-    G[idx] = Gin[i + (int64_t)j * ldg];
-    Z[idx] = (i == j) ? 1.0 : 0.0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
+  const double tol = 1e-14;
+  __shared__ double floor_s;
+  double dmax = 0.0;
+  for (int j = ty; j < b; j += 32)
+    for (int i = tx; i < b; i += 32) {
+      if (i <= j) {
+        const double v = Gin[i + j * ldg];            // upper triangle of the projected matrix
+        G[gidx(i, j)] = v;
+        if (i == j) dmax = fmax(dmax, fabs(v));
+      }
+      Z[i + j * b] = (i == j) ? 1.0 : 0.0;
+    }
+  dmax = warp_max(dmax);
+  if (tx == 0) red[ty] = dmax;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+    floor_s = 4.0 * 2.220446049250313e-16 * v;      // rounding floor: |g_pq| below it is noise
   }
   __syncthreads();
+  const double gfloor = floor_s;
+  const int bp = (b + 1) & ~1;      // even; index b is a dummy when b is odd
+  const int half = bp >> 1;
   int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) any_rot = 0;
+  for (; sweep <= max_sweeps; ++sweep) {
+    // convergence check: max_{i<j} |g_ij| / sqrt(|g_ii g_jj|)
+    double mx = 0.0;
+    for (int j = ty; j < b; j += 32)
+      for (int i = tx; i < j; i += 32) {
+        double g = fabs(G[gidx(i, j)]);
+        double dd = sqrt(fabs(G[gidx(i, i)] * G[gidx(j, j)]));
+        mx = fmax(mx, (g > gfloor) ? g / fmax(dd, 1e-300) : 0.0);
+      }
+    mx = warp_max(mx);
+    if (tx == 0) red[ty] = mx;
     __syncthreads();
+    if (ty == 0) {
+      double v = red[tx];
+      v = warp_max(v);
+      if (tx == 0) red[0] = v;
+    }
+    __syncthreads();
+    const bool done = red[0] <= tol;
+    __syncthreads();
+    if (done || sweep == max_sweeps) break;
     for (int r = 0; r < bp - 1; ++r) {
       if (tid < half) {
-        int m = tid;
-        int a = (m == 0) ? 0 : ((m - 1 + r) % (bp - 1)) + 1;
-        int mm = bp - 1 - m;
-        int q = ((mm - 1 + r) % (bp - 1)) + 1;
-        int p = a;
-        if (p > q) { int tmp = p; p = q; q = tmp; }
+        const int m = tid;
+        const int a = (m == 0) ? 0 : ((m - 1 + r) % (bp - 1)) + 1;
+        const int q0 = ((bp - 2 - m + r) % (bp - 1)) + 1;     // position bp-1-m
+        const int p = min(a, q0), q = max(a, q0);
         double c = 1.0, s = 0.0, t = 0.0;
         int rot = 0;
         if (q < b) {
-          double gpq = G[p + q * b];
-          double gpp = G[p + p * b], gqq = G[q + q * b];
-          if (fabs(gpq) > 1e-14 * sqrt(fabs(gpp * gqq)) && fabs(gpq) > 1e-300) {
-            double th = (gqq - gpp) / (2.0 * gpq);
-            double tt;
-            if (fabs(th) > 1e150) tt = 0.5 / th;
-            else tt = copysign(1.0, th) / (fabs(th) + sqrt(1.0 + th * th));
-            t = tt;
-            c = 1.0 / sqrt(1.0 + tt * tt);
-            s = tt * c;
+          const double gpq = G[gidx(p, q)];
+          const double gpp = G[gidx(p, p)], gqq = G[gidx(q, q)];
+          if (fabs(gpq) > tol * sqrt(fabs(gpp * gqq)) && fabs(gpq) > gfloor) {
+            const double th = (gqq - gpp) / (2.0 * gpq);
+            t = (fabs(th) > 1e150) ? 0.5 / th : copysign(1.0, th) / (fabs(th) + sqrt(1.0 + th * th));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
             rot = 1;
           }
         }
         cs_p[m] = p; cs_q[m] = q; cs_c[m] = c; cs_s[m] = s; cs_t[m] = t; cs_rot[m] = rot;
-        if (rot) any_rot = 1;
       }
       __syncthreads();
-      // G <- J^T G J on all 2x2 blocks touched by a rotation
-      const int nblk = half * half;
-      for (int idx = tid; idx < nblk; idx += nt) {
-        int m1 = idx / half, m2 = idx % half;
-        if (!cs_rot[m1] && !cs_rot[m2]) continue;
-        int p1 = cs_p[m1], q1 = cs_q[m1], p2 = cs_p[m2], q2 = cs_q[m2];
-        if (m1 == m2) {
-          if (q1 < b) {
-            double gpq = G[p1 + q1 * b], t = cs_t[m1];
-            G[p1 + p1 * b] -= t * gpq;
-            G[q1 + q1 * b] += t * gpq;
-            G[p1 + q1 * b] = 0.0;
-            G[q1 + p1 * b] = 0.0;
+      // G <- J^T G J on the 2x2 blocks (m1 <= m2) touched by a rotation
+      for (int m1 = ty; m1 < half; m1 += 32) {
+        const int r1 = cs_rot[m1];
+        const int p1 = cs_p[m1], q1 = cs_q[m1];
+        const double c1 = cs_c[m1], s1 = cs_s[m1];
+        for (int m2 = tx; m2 < half; m2 += 32) {
+          if (m2 < m1 || (!r1 && !cs_rot[m2])) continue;
+          if (m2 == m1) {
+            if (q1 < b) {
+              const int ipq = gidx(p1, q1);
+              const double gpq = G[ipq], t = cs_t[m1];
+              G[gidx(p1, p1)] -= t * gpq;
+              G[gidx(q1, q1)] += t * gpq;
+              G[ipq] = 0.0;
+            }
+            continue;
           }
-          continue;
+          const int p2 = cs_p[m2], q2 = cs_q[m2];
+          const double c2 = cs_c[m2], s2 = cs_s[m2];
+          const bool hq1 = q1 < b, hq2 = q2 < b;
+          const int ia = gidx(p1, p2);
+          const int ib = hq2 ? gidx(p1, q2) : 0;
+          const int ic = hq1 ? gidx(q1, p2) : 0;
+          const int id = (hq1 && hq2) ? gidx(q1, q2) : 0;
+          const double a = G[ia];
+          const double bb = hq2 ? G[ib] : 0.0;
+          const double cc = hq1 ? G[ic] : 0.0;
+          const double d = (hq1 && hq2) ? G[id] : 0.0;
+          const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;     // columns p2, q2
+          const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
+          G[ia] = c1 * a2 - s1 * c2v;                                     // rows p1, q1
+          if (hq2) G[ib] = c1 * b2 - s1 * d2;
+          if (hq1) G[ic] = s1 * a2 + c1 * c2v;
+          if (hq1 && hq2) G[id] = s1 * b2 + c1 * d2;
         }
-        double c1 = cs_c[m1], s1 = cs_s[m1], c2 = cs_c[m2], s2 = cs_s[m2];
-        bool hq1 = q1 < b, hq2 = q2 < b;
-        double a = G[p1 + p2 * b];
-        double bb = hq2 ? G[p1 + q2 * b] : 0.0;
-        double cc = hq1 ? G[q1 + p2 * b] : 0.0;
-        double d = (hq1 && hq2) ? G[q1 + q2 * b] : 0.0;
-        double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;      // right: columns p2, q2
-        double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
-        G[p1 + p2 * b] = c1 * a2 - s1 * c2v;                        // left: rows p1, q1
-        if (hq2) G[p1 + q2 * b] = c1 * b2 - s1 * d2;
-        if (hq1) G[q1 + p2 * b] = s1 * a2 + c1 * c2v;
-        if (hq1 && hq2) G[q1 + q2 * b] = s1 * b2 + c1 * d2;
       }
-      // Z <- Z J
-      const int nz = b * half;
-      for (int idx = tid; idx < nz; idx += nt) {
-        int m = idx / b, x = idx % b;
+      // Z <- Z J (column pairs)
+      for (int m = ty; m < half; m += 32) {
         if (!cs_rot[m]) continue;
-        int p = cs_p[m], q = cs_q[m];
-        double c = cs_c[m], s = cs_s[m];
-        double zp = Z[x + p * b], zq = Z[x + q * b];
-        Z[x + p * b] = c * zp - s * zq;
-        Z[x + q * b] = s * zp + c * zq;
+        const int p = cs_p[m], q = cs_q[m];
+        const double c = cs_c[m], s = cs_s[m];
+        for (int x = tx; x < b; x += 32) {
+          const double zp = Z[x + p * b], zq = Z[x + q * b];
+          Z[x + p * b] = c * zp - s * zq;
+          Z[x + q * b] = s * zp + c * zq;
+        }
       }
       __syncthreads();
     }
-    if (!any_rot) break;
-    __syncthreads();
   }
   if (tid == 0 && ctrl && sweep >= max_sweeps) ctrl->nonfinite |= 2;
   // ascending order (ties by index)
-  for (int i = tid; i < b; i += nt) diag_s[i] = G[i + i * b];
+  for (int i = tid; i < b; i += 1024) diag_s[i] = G[gidx(i, i)];
   __syncthreads();
-  for (int i = tid; i < b; i += nt) {
-    double v = diag_s[i];
+  for (int i = tid; i < b; i += 1024) {
+    const double v = diag_s[i];
     int rk = 0;
     for (int j = 0; j < b; ++j) {
-      double w = diag_s[j];
+      const double w = diag_s[j];
       rk += (w < v) || (w == v && j < i);
     }
     rank_s[i] = rk;
     theta_out[rk] = v;
   }
   __syncthreads();
-  for (int idx = tid; idx < b * b; idx += nt) {
-    int x = idx % b, i = idx / b;
-    Zout[x + (int64_t)rank_s[i] * b] = Z[idx];
-  }
+  for (int i = ty; i < b; i += 32)
+    for (int x = tx; x < b; x += 32) Zout[x + (int64_t)rank_s[i] * b] = Z[x + i * b];
 }
 
 // ----------------------------------------------------------------- lock ----
@@ -231,31 +278,43 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Gin,
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
                        const double* __restrict__ wn, double* __restrict__ rel, int b, int L,
                        double tol, Ctrl* ctrl, double* fp) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int kL = ctrl->kL;
-  ctrl->kL_prev = kL;
-  for (int j = kL; j < b; ++j) {
-    double r = res[j] / wn[j];
-    rel[j] = r;
-    if (!isfinite(r)) ctrl->nonfinite |= 1;
+  const int lane = threadIdx.x;            // one warp
+  const int kL = ctrl->kL;
+  int first_bad = b, nonfin = 0;
+  for (int base = kL; base < b; base += 32) {
+    const int j = base + lane;
+    bool bad = false;
+    if (j < b) {
+      const double r = res[j] / wn[j];
+      rel[j] = r;
+      nonfin |= !isfinite(r);
+      bad = !(r <= tol);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, bad);
+    if (m && first_bad == b) first_bad = base + __ffs(m) - 1;   // contiguous run from the bottom (R15)
   }
-  int j = kL;
-  while (j < b && rel[j] <= tol) ++j;     // contiguous run from the bottom (R15)
-  ctrl->kL = j;
+  nonfin = __any_sync(0xffffffffu, nonfin);
+  __syncwarp();
   double mx = 0.0;
-  for (int i = 0; i < min(L, b); ++i) mx = fmax(mx, rel[i]);
-  ctrl->max_rel = mx;
-  if (j < b) {
-    double lam = theta[j];                // scale point: smallest non-locked Ritz value (R9)
-    double alpha = theta[b - 1];          // damped interval [alpha, beta] (R9, R10)
-    double beta = ctrl->beta;
-    double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
-    if (!(e > 0.0)) e = fmax(fabs(beta), 1.0) * 1e-12;
-    ctrl->lambda = lam;
-    ctrl->alpha = alpha;
-    fp[0] = lam;
-    fp[1] = c;
-    fp[2] = e;
+  for (int i = lane; i < min(L, b); i += 32) mx = fmax(mx, rel[i]);
+  mx = warp_max(mx);
+  if (lane == 0) {
+    ctrl->kL_prev = kL;
+    ctrl->kL = first_bad;
+    ctrl->max_rel = mx;
+    if (nonfin) ctrl->nonfinite |= 1;
+    if (first_bad < b) {
+      const double lam = theta[first_bad];  // scale point: smallest non-locked Ritz value (R9)
+      const double alpha = theta[b - 1];    // damped interval [alpha, beta] (R9, R10)
+      const double beta = ctrl->beta;
+      double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
+      if (!(e > 0.0)) e = fmax(fabs(beta), 1.0) * 1e-12;
+      ctrl->lambda = lam;
+      ctrl->alpha = alpha;
+      fp[0] = lam;
+      fp[1] = c;
+      fp[2] = e;
+    }
   }
 }
 
@@ -351,15 +410,20 @@ __global__ void __launch_bounds__(256) k_gather_sign(const double* __restrict__ 
 // ------------------------------------------------------------------ host ----
 static int g_small_attr = 0;
 
-static int set_small_attrs() {
+constexpr int CHOL_SMEM_MAX_B = 156;    // b*b*8 <= ~195 KB
+constexpr int JAC_SMEM_MAX_B = 133;     // (b(b+1)/2 + b*b)*8 <= ~213 KB
+
+static size_t jac_smem(int b) { return (size_t)((((b * (b + 1)) >> 1) + 1) & ~1) * 8 + (size_t)b * b * 8; }
+
+int set_small_attrs() {
   if (g_small_attr) return SCSF_OK;
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       CHOL_SMEM_MAX_B * CHOL_SMEM_MAX_B * 8));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)jac_smem(JAC_SMEM_MAX_B)));
   g_small_attr = 1;
   return SCSF_OK;
 }
-
-constexpr int SMALL_SMEM_MAX_B = 156;   // b*b*8 <= ~195 KB
 
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
                   Ctrl* ctrl, cudaStream_t s) {
@@ -368,7 +432,7 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(set_small_attrs());
-  if (b <= SMALL_SMEM_MAX_B)
+  if (b <= CHOL_SMEM_MAX_B)
     k_chol_inv<true><<<1, 1024, (size_t)b * b * sizeof(double), s>>>(S, lds, b, nrows, Rinv, scratch, ctrl);
   else
     k_chol_inv<false><<<1, 1024, 0, s>>>(S, lds, b, nrows, Rinv, scratch, ctrl);
@@ -376,6 +440,7 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
   return SCSF_OK;
 }
 
+// scratchG: >= b(b+1)/2 + 1 doubles; Z: b*b doubles (global fallback only)
 int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
                 double* Zout, Ctrl* ctrl, cudaStream_t s) {
   if (b > 384) {
@@ -383,10 +448,10 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(set_small_attrs());
-  if (b <= SMALL_SMEM_MAX_B)
-    k_jacobi<true><<<1, 1024, (size_t)b * b * sizeof(double), s>>>(G, ldg, b, scratchG, Z, theta, Zout, 60, ctrl);
+  if (b <= JAC_SMEM_MAX_B)
+    k_jacobi<true><<<1, 1024, jac_smem(b), s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);
   else
-    k_jacobi<false><<<1, 1024, 0, s>>>(G, ldg, b, scratchG, Z, theta, Zout, 60, ctrl);
+    k_jacobi<false><<<1, 1024, 0, s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

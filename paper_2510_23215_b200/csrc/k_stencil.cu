@@ -145,23 +145,152 @@ __global__ void __launch_bounds__(ST_THREADS) k_stencil(
   }
 }
 
+// Vectorised variant: 4 consecutive points per thread, 256-bit loads/stores of
+// the column streams (Y_s, Y_{s-1}, Y_{s+1}) and the coefficient arrays;
+// x-neighbours k-1 / k+4 as scalars (same cache lines), y/z-neighbours as
+// aligned 256-bit loads (requires nx % 4 == 0, checked on the host).  The
+// coefficients of a quad stay in registers across the CB columns of the CTA.
+// Points k >= n (the ld padding) are written as 0 so padding never holds NaN.
+constexpr int SV_THREADS = 128;
+
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256).  ldg4_nc only for data
+// that is read-only for the whole kernel (coefficients, X).
+__device__ __forceinline__ double4 ldg4_nc(const double* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double4 ldg4(const double* p) {
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg4(double* p, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+               : "memory");
+}
+
+template <int DIM, int CB>
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
+    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n,
+    const double* __restrict__ X, const double* Xp, double* Out,   // Out may alias Xp (same-index RMW)
+    int64_t ldv, int ncols, const double* __restrict__ fp, int step) {
+  const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
+  if (k0 >= ldv) return;
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int64_t sxy = (int64_t)nx * ny;
+  const int j0 = blockIdx.y * CB;
+  const int j1 = min(ncols, j0 + CB);
+  if (k0 + 4 <= n) {
+    const double4 dg = ldg4_nc(cf + k0);
+    const double4 cxp = ldg4_nc(cf + ldc + k0);
+    const double cxm = (k0 >= 1) ? cf[ldc + k0 - 1] : 0.0;
+    const double4 cyp = ldg4_nc(cf + 2 * ldc + k0);
+    const bool hym = k0 >= nx, hyp = k0 + nx + 3 < n;
+    const double4 cym = hym ? ldg4_nc(cf + 2 * ldc + k0 - nx) : make_double4(0, 0, 0, 0);
+    double4 czp = make_double4(0, 0, 0, 0), czm = make_double4(0, 0, 0, 0);
+    bool hzm = false, hzp = false;
+    if (DIM == 3) {
+      czp = ldg4_nc(cf + 3 * ldc + k0);
+      hzm = k0 >= sxy;
+      hzp = k0 + sxy + 3 < n;
+      if (hzm) czm = ldg4_nc(cf + 3 * ldc + k0 - sxy);
+    }
+    const bool hm = k0 >= 1, hp = k0 + 4 < n;
+#pragma unroll 2
+    for (int j = j0; j < j1; ++j) {
+      const double* __restrict__ x = X + (int64_t)j * ldv;
+      const double4 xc = ldg4_nc(x + k0);
+      const double xl = hm ? x[k0 - 1] : 0.0;
+      const double xr = hp ? x[k0 + 4] : 0.0;
+      const double4 xu = hyp ? ldg4_nc(x + k0 + nx) : make_double4(0, 0, 0, 0);
+      const double4 xd = hym ? ldg4_nc(x + k0 - nx) : make_double4(0, 0, 0, 0);
+      double4 v;
+      v.x = (dg.x - c) * xc.x + cxp.x * xc.y + cxm * xl + cyp.x * xu.x + cym.x * xd.x;
+      v.y = (dg.y - c) * xc.y + cxp.y * xc.z + cxp.x * xc.x + cyp.y * xu.y + cym.y * xd.y;
+      v.z = (dg.z - c) * xc.z + cxp.z * xc.w + cxp.y * xc.y + cyp.z * xu.z + cym.z * xd.z;
+      v.w = (dg.w - c) * xc.w + cxp.w * xr + cxp.z * xc.z + cyp.w * xu.w + cym.w * xd.w;
+      if (DIM == 3) {
+        const double4 zu = hzp ? ldg4_nc(x + k0 + sxy) : make_double4(0, 0, 0, 0);
+        const double4 zd = hzm ? ldg4_nc(x + k0 - sxy) : make_double4(0, 0, 0, 0);
+        v.x += czp.x * zu.x + czm.x * zd.x;
+        v.y += czp.y * zu.y + czm.y * zd.y;
+        v.z += czp.z * zu.z + czm.z * zd.z;
+        v.w += czp.w * zu.w + czm.w * zd.w;
+      }
+      v.x *= a; v.y *= a; v.z *= a; v.w *= a;
+      if (b != 0.0) {
+        const double4 p = ldg4(Xp + (int64_t)j * ldv + k0);
+        v.x = fma(b, p.x, v.x); v.y = fma(b, p.y, v.y); v.z = fma(b, p.z, v.z); v.w = fma(b, p.w, v.w);
+      }
+      stg4(Out + (int64_t)j * ldv + k0, v);
+    }
+    return;
+  }
+  // tail quad (n % 4 != 0) and padding: scalar, guarded
+  for (int q = 0; q < 4; ++q) {
+    const int64_t k = k0 + q;
+    if (k >= ldv) break;
+    if (k >= n) {
+      for (int j = j0; j < j1; ++j) Out[(int64_t)j * ldv + k] = 0.0;
+      continue;
+    }
+    const double dg = cf[k] - c;
+    const double xp = cf[ldc + k], xm = (k >= 1) ? cf[ldc + k - 1] : 0.0;
+    const double yp = cf[2 * ldc + k], ym = (k >= nx) ? cf[2 * ldc + k - nx] : 0.0;
+    double zp = 0.0, zm = 0.0;
+    if (DIM == 3) {
+      zp = cf[3 * ldc + k];
+      zm = (k >= sxy) ? cf[3 * ldc + k - sxy] : 0.0;
+    }
+    for (int j = j0; j < j1; ++j) {
+      const double* x = X + (int64_t)j * ldv;
+      double v = dg * x[k];
+      if (k + 1 < n) v = fma(xp, x[k + 1], v);
+      if (k >= 1) v = fma(xm, x[k - 1], v);
+      if (k + nx < n) v = fma(yp, x[k + nx], v);
+      if (k >= nx) v = fma(ym, x[k - nx], v);
+      if (DIM == 3) {
+        if (k + sxy < n) v = fma(zp, x[k + sxy], v);
+        if (k >= sxy) v = fma(zm, x[k - sxy], v);
+      }
+      v *= a;
+      if (b != 0.0) v = fma(b, Xp[(int64_t)j * ldv + k], v);
+      Out[(int64_t)j * ldv + k] = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------- residuals ----
 // For active column j: res[j] = ||W_j - theta_j V_j||_2, wn[j] = ||W_j||_2 (fixed-order sums).
-__global__ void __launch_bounds__(256) k_resid(const double* __restrict__ V, const double* __restrict__ W,
+__global__ void __launch_bounds__(512) k_resid(const double* __restrict__ V, const double* __restrict__ W,
                                                int64_t ldv, int64_t n, const double* __restrict__ theta,
                                                double* __restrict__ res, double* __restrict__ wn) {
-  int j = blockIdx.x;
+  const int j = blockIdx.x;
   const double* v = V + (int64_t)j * ldv;
   const double* w = W + (int64_t)j * ldv;
-  double th = theta[j];
+  const double th = theta[j];
   double r2 = 0.0, w2 = 0.0;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-    double wk = w[k];
-    double d = fma(-th, v[k], wk);
-    r2 = fma(d, d, r2);
-    w2 = fma(wk, wk, w2);
+  const int64_t n2 = n & ~(int64_t)1;                 // ld is even: 16-byte aligned pairs
+#pragma unroll 4
+  for (int64_t k = 2 * threadIdx.x; k < n2; k += 2 * blockDim.x) {
+    const double2 wk = *reinterpret_cast<const double2*>(w + k);
+    const double2 vk = *reinterpret_cast<const double2*>(v + k);
+    const double d0 = fma(-th, vk.x, wk.x), d1 = fma(-th, vk.y, wk.y);
+    r2 = fma(d0, d0, r2);
+    r2 = fma(d1, d1, r2);
+    w2 = fma(wk.x, wk.x, w2);
+    w2 = fma(wk.y, wk.y, w2);
   }
-  __shared__ double sr[8], sw[8];
+  if (threadIdx.x == 0 && n2 < n) {
+    const double d = fma(-th, v[n - 1], w[n - 1]);
+    r2 = fma(d, d, r2);
+    w2 = fma(w[n - 1], w[n - 1], w2);
+  }
+  __shared__ double sr[16], sw[16];
   r2 = warp_sum(r2);
   w2 = warp_sum(w2);
   if ((threadIdx.x & 31) == 0) {
@@ -170,13 +299,13 @@ __global__ void __launch_bounds__(256) k_resid(const double* __restrict__ V, con
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < 8; ++i) {
+    double a = 0.0, bb = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
       a += sr[i];
-      b += sw[i];
+      bb += sw[i];
     }
     res[j] = sqrt(a);
-    wn[j] = sqrt(b);
+    wn[j] = sqrt(bb);
   }
 }
 
@@ -206,11 +335,23 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
   if (ncols <= 0) return SCSF_OK;
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
   const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
-  dim3 g(ceil_div(n, ST_THREADS), ceil_div(ncols, ST_COLS));
-  if (ops->dim == 2)
-    k_stencil<2><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
-  else
-    k_stencil<3><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+  const bool vec = (ops->nx % 4 == 0) && (ldv % 4 == 0) && (ops->ld % 4 == 0) &&
+                   ((uintptr_t)X % 32 == 0) && ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0) &&
+                   (Xp == nullptr || (uintptr_t)Xp % 32 == 0);
+  if (vec) {
+    constexpr int CB = 4;
+    dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
+    if (ops->dim == 2)
+      k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+    else
+      k_stencil_v4<3, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+  } else {
+    dim3 g(ceil_div(n, ST_THREADS), ceil_div(ncols, ST_COLS));
+    if (ops->dim == 2)
+      k_stencil<2><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+    else
+      k_stencil<3><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+  }
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
@@ -218,7 +359,7 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
 int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
                const double* theta, double* res, double* wn, cudaStream_t s) {
   if (ncols <= 0) return SCSF_OK;
-  k_resid<<<ncols, 256, 0, s>>>(V, W, ldv, n, theta, res, wn);
+  k_resid<<<ncols, 512, 0, s>>>(V, W, ldv, n, theta, res, wn);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

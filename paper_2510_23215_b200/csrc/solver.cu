@@ -29,6 +29,8 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
             double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s);
 int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
             double alpha, double beta, double* Out, int64_t ldo, cudaStream_t s);
+int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+               double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s);
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
                   Ctrl* ctrl, cudaStream_t s);
@@ -90,7 +92,7 @@ int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_byte
 static int cholqr_pass(SolveWS& w, double* Y, double* Out, int ncols, cudaStream_t s) {
   SCSF_TRY(gemm_tn(Y, w.ldv, ncols, Y, w.ldv, ncols, w.n, 1.0, 1, w.S, ncols, w.P, s));
   SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n, w.Rinv, w.Gwork, w.ctrl, s));
-  SCSF_TRY(gemm_nn(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, s));
+  SCSF_TRY(gemm_nn_ex(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, 1, s));
   return SCSF_OK;
 }
 

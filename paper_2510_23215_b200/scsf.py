@@ -25,7 +25,8 @@ EXPORTED = [
     "scsf_sort_workspace_bytes", "scsf_sort", "scsf_signatures", "scsf_assemble",
     "scsf_filter_workspace_bytes", "scsf_cheb_filter", "scsf_solve_workspace_bytes",
     "scsf_solve_one", "scsf_solve_queue", "scsf_last_error", "scsf_abi_version",
-    "scsf_launch_count", "scsf_set_timing",
+    "scsf_launch_count", "scsf_set_timing", "scsf_solve_chains",
+    "scsf_dev_workspace_bytes", "scsf_gemm_tn", "scsf_gemm_nn", "scsf_chol_inv", "scsf_syev_small",
 ]
 
 
@@ -87,6 +88,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_abi_version": (ctypes.c_int, []),
         "scsf_launch_count": (ctypes.c_int64, []),
         "scsf_set_timing": (ctypes.c_int, [I32]),
+        "scsf_solve_chains": (ctypes.c_int, [OPS, P, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P, I64,
+                                             ST, P, SZ, P]),
+        "scsf_dev_workspace_bytes": (SZ, [I64, I32, I32]),
+        "scsf_gemm_tn": (ctypes.c_int, [P, I64, I32, P, I64, I32, I64, D, I32, P, I64, P, SZ, P]),
+        "scsf_gemm_nn": (ctypes.c_int, [P, I64, I64, I32, P, I64, I32, D, D, P, I64, P]),
+        "scsf_chol_inv": (ctypes.c_int, [P, I64, I32, I64, P, P, SZ, P]),
+        "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -271,3 +279,88 @@ def solve_queue(ops: Operators, chain, L: int, nex: int, degree: int = 20, tol: 
     if raise_on_fail or code != SCSF_ERR_NUMERICAL:
         _check(code)
     return evals, (evecs if want_vecs else None), [stats[i].as_dict() for i in range(nc)]
+
+
+def split_chains(length: int, n_chains: int) -> np.ndarray:
+    """chain_start offsets of n_chains contiguous, near-equal slices of a queue."""
+    n_chains = max(1, min(n_chains, max(length, 1)))
+    return np.array([(c * length) // n_chains for c in range(n_chains + 1)], dtype=np.int32)
+
+
+def solve_chains(ops: Operators, queue, n_chains: int, L: int, nex: int, degree: int = 20, tol: float = 1e-8,
+                 max_iter: int = 200, seed: int = 0, want_vecs: bool = True, raise_on_fail=True,
+                 ws: torch.Tensor | None = None, evals: torch.Tensor | None = None,
+                 evecs: torch.Tensor | None = None, chain_start=None):
+    """Concurrent warm-start chains over contiguous slices of `queue` (scsf_solve_chains).
+
+    Returns (evals[len, L], evecs[len, L, ld] or None, stats list) by queue position.
+    """
+    lib = load_library()
+    queue = np.ascontiguousarray(np.asarray(queue, dtype=np.int32))
+    nq = int(queue.shape[0])
+    starts = split_chains(nq, n_chains) if chain_start is None else np.ascontiguousarray(chain_start, dtype=np.int32)
+    nc = len(starts) - 1
+    st = ops.c_struct()
+    per = lib.scsf_solve_workspace_bytes(ctypes.byref(st), L, nex)
+    if ws is None:
+        ws = _workspace(per * nc, ops.coef.device)
+    dev = ops.coef.device
+    if evals is None:
+        evals = torch.empty((nq, L), dtype=torch.float64, device=dev)
+    if want_vecs and evecs is None:
+        evecs = torch.empty((nq, L, ops.ld), dtype=torch.float64, device=dev)
+    stats = (scsf_stats * max(nq, 1))()
+    code = lib.scsf_solve_chains(ctypes.byref(st), queue.ctypes.data_as(ctypes.c_void_p),
+                                 starts.ctypes.data_as(ctypes.c_void_p), nc, L, nex, degree, tol, max_iter,
+                                 ctypes.c_uint64(seed), _ptr(evals), _ptr(evecs) if want_vecs else None, ops.ld,
+                                 stats, _ptr(ws), ws.numel(), _stream())
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return evals, (evecs if want_vecs else None), [stats[i].as_dict() for i in range(nq)]
+
+
+# ------------------------------------------------------- component entries ----
+# Blocks are column-major: a torch tensor of shape [cols, ld] holds an ld x cols block.
+def gemm_tn(X: torch.Tensor, Y: torch.Tensor, n: int, alpha: float = 1.0, upper: bool = False) -> torch.Tensor:
+    """C = alpha X[:n]^T Y[:n] for X [b1, ldx], Y [b2, ldy]; returns C as [b2, b1] (column-major b1 x b2)."""
+    lib = load_library()
+    b1, ldx = X.shape
+    b2, ldy = Y.shape
+    ws = _workspace(lib.scsf_dev_workspace_bytes(n, b1, b2), X.device)
+    C = torch.zeros((b2, b1), dtype=torch.float64, device=X.device)
+    _check(lib.scsf_gemm_tn(_ptr(X), ldx, b1, _ptr(Y), ldy, b2, n, alpha, 1 if upper else 0, _ptr(C), b1,
+                            _ptr(ws), ws.numel(), _stream()))
+    return C
+
+
+def gemm_nn(X: torch.Tensor, M: torch.Tensor, n: int, alpha: float = 1.0, beta: float = 0.0,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    """Out = alpha X[:n] M + beta Out for X [b1, ldx], M [b2, b1] (column-major b1 x b2); out [b2, ldx]."""
+    lib = load_library()
+    b1, ldx = X.shape
+    b2, ldm = M.shape
+    if out is None:
+        out = torch.zeros((b2, ldx), dtype=torch.float64, device=X.device)
+    _check(lib.scsf_gemm_nn(_ptr(X), ldx, n, b1, _ptr(M), ldm, b2, alpha, beta, _ptr(out), out.shape[1], _stream()))
+    return out
+
+
+def chol_inv(S: torch.Tensor, nrows: int = 1):
+    """R^{-1} of S = R^T R (upper triangle of S used); S, result [b, b] column-major."""
+    lib = load_library()
+    b = S.shape[0]
+    ws = _workspace(lib.scsf_dev_workspace_bytes(1, b, b), S.device)
+    R = torch.empty_like(S)
+    _check(lib.scsf_chol_inv(_ptr(S), b, b, nrows, _ptr(R), _ptr(ws), ws.numel(), _stream()))
+    return R
+
+
+def syev_small(G: torch.Tensor):
+    """theta ascending, Z (column-major [b, b]) with G = Z diag(theta) Z^T (upper triangle of G used)."""
+    lib = load_library()
+    b = G.shape[0]
+    ws = _workspace(lib.scsf_dev_workspace_bytes(1, b, b), G.device)
+    theta = torch.empty(b, dtype=torch.float64, device=G.device)
+    Z = torch.empty_like(G)
+    _check(lib.scsf_syev_small(_ptr(G), b, b, _ptr(theta), _ptr(Z), _ptr(ws), ws.numel(), _stream()))
+    return theta, Z

@@ -28,7 +28,7 @@ def libpath():
 
 def test_header_declares_boundary():
     names = _declared()
-    for required in ("scsf_sort", "scsf_solve_one", "scsf_solve_queue"):
+    for required in ("scsf_sort", "scsf_solve_one", "scsf_solve_queue", "scsf_solve_chains"):
         assert required in names
 
 

@@ -226,3 +226,32 @@ def test_launch_count_increases(lib):
     before = lib.launch_count()
     lib.solve_one(ops, 0, 4, 1, 8, 1e-8, 100)
     assert lib.launch_count() > before
+
+
+def test_solve_chains_matches_single_chains_bitwise(lib):
+    """scsf_solve_chains runs contiguous slices concurrently; each slice must equal scsf_solve_queue
+    on the same slice bit for bit (deterministic kernels, no cross-chain state)."""
+    import torch
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 24)
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    starts = lib.split_chains(len(perm), 3)
+    ev, vec, st = lib.solve_chains(ops, perm, 3, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=11)
+    for c in range(3):
+        a, b = starts[c], starts[c + 1]
+        ev1, vec1, st1 = lib.solve_queue(ops, perm[a:b], cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=11)
+        assert torch.equal(ev[a:b], ev1) and torch.equal(vec[a:b], vec1)
+        assert [s["iterations"] for s in st[a:b]] == [s["iterations"] for s in st1]
+        assert st[a]["warm"] == 0 and all(s["warm"] == 1 for s in st[a + 1:b])
+    for k in (0, 7, 8, 23):
+        check_pairs(f, int(perm[k]), ev[k].cpu().numpy(), vec[k, :, :f.n].cpu().numpy().T, cfg.L,
+                    paper_tol=10 * cfg.tol)
+
+
+def test_solve_chains_more_chains_than_operators(lib):
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 3)
+    ops, _ = device_problem(f)
+    ev, vec, st = lib.solve_chains(ops, [2, 0, 1], 8, cfg.L, cfg.nex, seed=1)
+    assert all(s["status"] == 0 and s["warm"] == 0 for s in st)
