@@ -81,6 +81,8 @@ typedef struct {
   double t_ortho_ms;         /* BCGS2 against locked + CholQR2 (Alg. 3 l. 4)          */
   double t_rr_ms;            /* Rayleigh-Ritz + residuals + locking (ll. 5-7)          */
   double filter_bytes;       /* algorithmic HBM bytes of the filter steps */
+  int32_t jacobi_sweeps;     /* reduced-eigensolver sweeps, summed over RR steps      */
+  int32_t reserved0;
 } scsf_stats;
 
 /* ---------------------------------------------------------------- sort ---- */
@@ -225,6 +227,7 @@ int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* 
  *   SCSF_ERR_NUMERICAL if S needed the shifted fallback.
  * scsf_syev_small: G (b x b, upper triangle used) = Z diag(theta) Z^T, theta
  *   ascending (b), Z (b x b, ld b): the reduced eigenproblem (l. 6).
+ *   SCSF_ERR_NUMERICAL if the sweep cap was hit.
  */
 size_t scsf_dev_workspace_bytes(int64_t n, int32_t b1, int32_t b2);
 int scsf_gemm_tn(const double* X, int64_t ldx, int32_t b1, const double* Y, int64_t ldy, int32_t b2,
@@ -234,8 +237,8 @@ int scsf_gemm_nn(const double* X, int64_t ldx, int64_t n, int32_t b1, const doub
                  int32_t b2, double alpha, double beta, double* Out, int64_t ldo, void* stream);
 int scsf_chol_inv(const double* S, int64_t lds, int32_t b, int64_t nrows, double* Rinv, void* ws,
                   size_t ws_bytes, void* stream);
-int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z, void* ws,
-                    size_t ws_bytes, void* stream);
+int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z,
+                    int32_t* sweeps /* host out or NULL */, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------- helpers ---- */
 

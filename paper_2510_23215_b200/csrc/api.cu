@@ -418,8 +418,8 @@ int scsf_chol_inv(const double* S, int64_t lds, int32_t b, int64_t nrows, double
   return SCSF_OK;
 }
 
-int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z, void* ws, size_t ws_bytes,
-                    void* stream) {
+int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, double* Z, int32_t* sweeps, void* ws,
+                    size_t ws_bytes, void* stream) {
   SCSF_ARG_CHECK(G && theta && Z && b >= 1 && b <= 384 && ldg >= b, "bad syev_small arguments");
   Arena a(ws, ws_bytes);
   double* g = a.take<double>((int64_t)b * b + 2);
@@ -433,7 +433,14 @@ int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, doub
   cudaStream_t s = (cudaStream_t)stream;
   SCSF_CUDA_CHECK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
   SCSF_TRY(jacobi_impl(G, ldg, b, g, zw, theta, Z, ctrl, s));
+  Ctrl h{};
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (sweeps) *sweeps = h.pad[0];
+  if (h.nonfinite & 2) {
+    set_error("Jacobi did not converge within the sweep cap");
+    return SCSF_ERR_NUMERICAL;
+  }
   return SCSF_OK;
 }
 

@@ -84,19 +84,32 @@ __global__ void __launch_bounds__(128) k_gemm_tn(const double* __restrict__ X, i
       }
 }
 
-// C[i + j ldc] = alpha * sum_z P[z][i + j b1]  (z ascending, fixed order: deterministic).
-// Symmetric results (Gram, Rayleigh quotient) are symmetrised by their consumers on load.
-__global__ void k_reduce_partials(const double* __restrict__ P, int splits, int b1, int b2,
-                                  double alpha, double* __restrict__ C, int64_t ldc) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// C[i + j ldc] = alpha * sum_z P[z][i + j b1].  Warp w sums z = w, w+8, ... (ascending);
+// the 8 warp sums are then added in warp order: a fixed order, so deterministic.
+// Symmetric results (Gram, Rayleigh quotient) are read as upper triangles by their consumers.
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ P, int splits, int b1,
+                                                         int b2, double alpha, int upper, double* __restrict__ C,
+                                                         int64_t ldc) {
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   const int j = blockIdx.y;
-  if (i >= b1) return;
+  if (upper && blockIdx.x * 32 > j) return;          // tile strictly below the diagonal
   const int64_t stride = (int64_t)b1 * b2;
-  const double* p = P + i + (int64_t)j * b1;
   double s = 0.0;
-#pragma unroll 8
-  for (int z = 0; z < splits; ++z) s += __ldg(p + z * stride);
-  C[i + (int64_t)j * ldc] = alpha * s;
+  if (i < b1) {
+    const double* p = P + i + (int64_t)j * b1;
+#pragma unroll 4
+    for (int z = warp; z < splits; z += 8) s += __ldg(p + z * stride);
+  }
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && i < b1) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    C[i + (int64_t)j * ldc] = alpha * t;
+  }
 }
 
 // ------------------------------------------------------------- gemm_nn ----
@@ -394,11 +407,12 @@ int tn_splits(int64_t n, int b1, int b2) {
 }
 
 // Upper bound of splits * b1' * b2' over every call with b1' <= b1, b2' <= b2:
-// splits <= ceil(296 / tiles) and tiles >= b1' b2' / 64^2, so
-// splits * b1' * b2' <= 296 * 64^2 + b1' * b2'.
+// splits <= ceil(296 / tiles') where tiles' >= b1' b2' / 64^2 (full) or
+// >= (b1'/64)(b1'/64 + 1)/2 (upper-triangle mode, at least half of the full count), so
+// splits * b1' * b2' <= 2 * 296 * 64^2 + b1' * b2'.
 size_t tn_partial_doubles(int64_t n, int b1, int b2) {
   (void)n;
-  return (size_t)2 * 148 * TN_BM * TN_BM + (size_t)b1 * b2;
+  return (size_t)4 * 148 * TN_BM * TN_BM + (size_t)b1 * b2;
 }
 
 // C (b1 x b2, ldc) = alpha X^T Y.  P: workspace of tn_partial_doubles.
@@ -419,8 +433,8 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
   k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, P);
   SCSF_LAUNCH_CHECK();
-  dim3 gr(ceil_div(b1, 128), b2);
-  k_reduce_partials<<<gr, 128, 0, s>>>(P, splits, b1, b2, alpha, C, ldc);
+  dim3 gr(ceil_div(b1, 32), b2);
+  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper, C, ldc);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

@@ -254,7 +254,10 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Gin,
       __syncthreads();
     }
   }
-  if (tid == 0 && ctrl && sweep >= max_sweeps) ctrl->nonfinite |= 2;
+  if (tid == 0 && ctrl) {
+    if (sweep >= max_sweeps) ctrl->nonfinite |= 2;
+    ctrl->pad[0] += sweep;                            // cumulative Jacobi sweeps (stats)
+  }
   // ascending order (ties by index)
   for (int i = tid; i < b; i += 1024) diag_s[i] = G[gidx(i, i)];
   __syncthreads();
@@ -271,6 +274,185 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Gin,
   __syncthreads();
   for (int i = ty; i < b; i += 32)
     for (int x = tx; x < b; x += 32) Zout[x + (int64_t)rank_s[i] * b] = Z[x + i * b];
+}
+
+// ------------------------------------------------------ jacobi_eig (xor) ----
+// Same two-sided cyclic Jacobi, for b <= 128, with the "hypercube" parallel
+// ordering: round m = 1..B-1 (B = b rounded up to a power of two) rotates the
+// B/2 disjoint pairs (p, p ^ m); every pair occurs exactly once per sweep.
+// Z lives in registers: thread (warp w, lane l) owns rows x = w*S + sx and
+// columns p = l + 32 sp (S = B/32), so the partner column p ^ m is at lane
+// l ^ (m & 31), slot sp ^ (m >> 5): one __shfl_xor per element, no shared
+// memory traffic for Z.  G keeps only its upper triangle in shared memory
+// (pitch B + 1).  Indices >= b are inert (zero rows/columns, never rotated).
+template <int LOGB>
+__global__ void __launch_bounds__(1024, 1) k_jacobi_x(const double* __restrict__ Gin, int64_t ldg, int b,
+                                                      double* __restrict__ theta_out, double* __restrict__ Zout,
+                                                      int max_sweeps, Ctrl* ctrl) {
+  constexpr int B = 1 << LOGB;
+  constexpr int S = B / 32;
+  constexpr int GP = B + 1;
+  extern __shared__ double G[];                     // [B][GP], upper triangle used
+  __shared__ double cs_c[B], cs_s[B], cs_t[B];
+  __shared__ int cs_rot[B];
+  __shared__ int rank_s[B];
+  __shared__ double red[32];
+  __shared__ double floor_s;
+  __shared__ int any_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = 1e-14;
+  auto gi = [](int i, int j) { return (i <= j) ? i * GP + j : j * GP + i; };
+
+  // load the upper triangle (zero outside b), diagonal max for the rounding floor
+  double dmax = 0.0;
+  for (int idx = tid; idx < B * B; idx += 1024) {
+    const int i = idx >> LOGB, j = idx & (B - 1);
+    if (i <= j) {
+      const double v = (i < b && j < b) ? Gin[i + (int64_t)j * ldg] : 0.0;
+      G[i * GP + j] = v;
+      if (i == j) dmax = fmax(dmax, fabs(v));
+    }
+  }
+  dmax = warp_max(dmax);
+  if (lane == 0) red[warp] = dmax;
+  double z[S][S];
+#pragma unroll
+  for (int sx = 0; sx < S; ++sx)
+#pragma unroll
+    for (int sp = 0; sp < S; ++sp) z[sx][sp] = ((warp * S + sx) == (lane + 32 * sp)) ? 1.0 : 0.0;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+    floor_s = 4.0 * 2.220446049250313e-16 * v;
+  }
+  __syncthreads();
+  const double gfloor = floor_s;
+
+  int sweep = 0;
+  for (; sweep <= max_sweeps; ++sweep) {
+    double mx = 0.0;
+    for (int idx = tid; idx < B * B; idx += 1024) {
+      const int i = idx >> LOGB, j = idx & (B - 1);
+      if (i < j && j < b) {
+        const double g = fabs(G[i * GP + j]);
+        if (g > gfloor) mx = fmax(mx, g / fmax(sqrt(fabs(G[i * GP + i] * G[j * GP + j])), 1e-300));
+      }
+    }
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+      red[0] = v;
+    }
+    __syncthreads();
+    const bool done = red[0] <= tol;
+    __syncthreads();
+    if (done || sweep == max_sweeps) break;
+    for (int m = 1; m < B; ++m) {
+      const int h = 31 - __clz(m);                  // pairs: lo has bit h clear, hi = lo ^ m
+      if (tid == 0) any_rot = 0;
+      __syncthreads();
+      if (tid < B && !((tid >> h) & 1)) {
+        const int lo = tid, hi = tid ^ m;
+        double c = 1.0, s = 0.0, t = 0.0;
+        int rot = 0;
+        if (hi < b) {
+          const double gpq = G[lo * GP + hi], gpp = G[lo * GP + lo], gqq = G[hi * GP + hi];
+          if (fabs(gpq) > tol * sqrt(fabs(gpp * gqq)) && fabs(gpq) > gfloor) {
+            const double th = (gqq - gpp) / (2.0 * gpq);
+            t = (fabs(th) > 1e150) ? 0.5 / th : copysign(1.0, th) / (fabs(th) + sqrt(1.0 + th * th));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            rot = 1;
+            any_rot = 1;
+          }
+        }
+        cs_c[lo] = c; cs_s[lo] = s; cs_t[lo] = t; cs_rot[lo] = rot;
+      }
+      __syncthreads();
+      if (!any_rot) continue;                       // uniform: nothing to apply this round
+      // ---- G <- J^T G J on blocks {i_lo, i_hi} x {j_lo, j_hi}, i_lo <= j_lo (upper storage)
+      constexpr int H2 = B / 2;
+      const int lowmask = (1 << h) - 1;
+      for (int beta = tid; beta < H2 * H2; beta += 1024) {
+        const int ai = beta / H2, aj = beta % H2;
+        const int ilo = ((ai & ~lowmask) << 1) | (ai & lowmask);   // insert a 0 bit at position h
+        const int jlo = ((aj & ~lowmask) << 1) | (aj & lowmask);
+        if (ilo > jlo) continue;
+        const int r1 = cs_rot[ilo], r2 = cs_rot[jlo];
+        if (!r1 && !r2) continue;
+        const int ihi = ilo ^ m, jhi = jlo ^ m;
+        if (ilo == jlo) {
+          const int ipq = ilo * GP + ihi;
+          const double gpq = G[ipq], t = cs_t[ilo];
+          G[ilo * GP + ilo] -= t * gpq;
+          G[ihi * GP + ihi] += t * gpq;
+          G[ipq] = 0.0;
+          continue;
+        }
+        const double c1 = cs_c[ilo], s1 = cs_s[ilo], c2 = cs_c[jlo], s2 = cs_s[jlo];
+        const int ia = gi(ilo, jlo), ib = gi(ilo, jhi), ic = gi(ihi, jlo), id = gi(ihi, jhi);
+        const double a = G[ia], bb = G[ib], cc = G[ic], d = G[id];
+        const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;    // columns j_lo, j_hi
+        const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
+        G[ia] = c1 * a2 - s1 * c2v;                                   // rows i_lo, i_hi
+        G[ib] = c1 * b2 - s1 * d2;
+        G[ic] = s1 * a2 + c1 * c2v;
+        G[id] = s1 * b2 + c1 * d2;
+      }
+      // ---- Z <- Z J in registers
+      const int lm = m & 31, sm = m >> 5;
+#pragma unroll
+      for (int sx = 0; sx < S; ++sx) {
+        double q[S];
+#pragma unroll
+        for (int sp = 0; sp < S; ++sp) {
+          double src = z[sx][sp];                 // z[sx][sp ^ sm] with static register indices only
+#pragma unroll
+          for (int k = 1; k < S; ++k)
+            if (sm == k) src = z[sx][sp ^ k];
+          q[sp] = __shfl_xor_sync(0xffffffffu, src, lm);
+        }
+#pragma unroll
+        for (int sp = 0; sp < S; ++sp) {
+          const int pcol = lane + 32 * sp;
+          const int partner = pcol ^ m;
+          const int lo = min(pcol, partner);
+          if (cs_rot[lo]) {
+            const double c = cs_c[lo], s = cs_s[lo];
+            z[sx][sp] = (pcol < partner) ? (c * z[sx][sp] - s * q[sp]) : (s * q[sp] + c * z[sx][sp]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0 && ctrl) {
+    if (sweep >= max_sweeps) ctrl->nonfinite |= 2;
+    ctrl->pad[0] += sweep;
+  }
+  // ascending order of the b real eigenvalues (ties by index)
+  if (tid < b) {
+    const double v = G[tid * GP + tid];
+    int rk = 0;
+    for (int j = 0; j < b; ++j) {
+      const double w = G[j * GP + j];
+      rk += (w < v) || (w == v && j < tid);
+    }
+    rank_s[tid] = rk;
+    theta_out[rk] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int sx = 0; sx < S; ++sx)
+#pragma unroll
+    for (int sp = 0; sp < S; ++sp) {
+      const int x = warp * S + sx, pc = lane + 32 * sp;
+      if (x < b && pc < b) Zout[x + (int64_t)rank_s[pc] * b] = z[sx][sp];
+    }
 }
 
 // ----------------------------------------------------------------- lock ----
@@ -327,6 +509,7 @@ __global__ void k_ctrl_init(Ctrl* ctrl, const unsigned long long* gersh) {
   ctrl->chol_fallbacks = 0;
   ctrl->nonfinite = 0;
   ctrl->max_rel = 0.0;
+  ctrl->pad[0] = 0;
 }
 
 // ----------------------------------------------------------- rand_block ----
@@ -421,6 +604,8 @@ int set_small_attrs() {
                                        CHOL_SMEM_MAX_B * CHOL_SMEM_MAX_B * 8));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)jac_smem(JAC_SMEM_MAX_B)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_x<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       128 * 129 * (int)sizeof(double)));
   g_small_attr = 1;
   return SCSF_OK;
 }
@@ -448,7 +633,13 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(set_small_attrs());
-  if (b <= JAC_SMEM_MAX_B)
+  if (b <= 32)
+    k_jacobi_x<5><<<1, 1024, 32 * 33 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
+  else if (b <= 64)
+    k_jacobi_x<6><<<1, 1024, 64 * 65 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
+  else if (b <= 128)
+    k_jacobi_x<7><<<1, 1024, 128 * 129 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
+  else if (b <= JAC_SMEM_MAX_B)
     k_jacobi<true><<<1, 1024, jac_smem(b), s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);
   else
     k_jacobi<false><<<1, 1024, 0, s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);

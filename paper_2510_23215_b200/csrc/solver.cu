@@ -154,9 +154,20 @@ struct PhaseTimer {
   }
 };
 
+// Per-iteration host read of the control block.  The wait is a blocking-sync
+// event (the host thread sleeps instead of spinning), so many concurrent chain
+// threads do not compete for host cores.
+static thread_local cudaEvent_t t_ev = nullptr;
+static thread_local Ctrl* t_pinned = nullptr;
 static int read_ctrl(const SolveWS& w, Ctrl& h, cudaStream_t s) {
-  SCSF_CUDA_CHECK(cudaMemcpyAsync(&h, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (!t_ev) {
+    SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&t_ev, cudaEventBlockingSync | cudaEventDisableTiming));
+    SCSF_CUDA_CHECK(cudaMallocHost(&t_pinned, sizeof(Ctrl)));
+  }
+  SCSF_CUDA_CHECK(cudaMemcpyAsync(t_pinned, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+  SCSF_CUDA_CHECK(cudaEventRecord(t_ev, s));
+  SCSF_CUDA_CHECK(cudaEventSynchronize(t_ev));
+  h = *t_pinned;
   return SCSF_OK;
 }
 
@@ -256,6 +267,7 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
     st->t_ortho_ms = tm.ortho;
     st->t_rr_ms = tm.rr;
     st->filter_bytes = filter_bytes;
+    st->jacobi_sweeps = h.pad[0];
   }
   if (status != SCSF_OK)
     set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op,

@@ -52,7 +52,8 @@ class scsf_stats(ctypes.Structure):
                 ("n_locked", ctypes.c_int32), ("warm", ctypes.c_int32),
                 ("spmm_columns", ctypes.c_int64), ("max_rel_resid", ctypes.c_double),
                 ("beta", ctypes.c_double), ("t_filter_ms", ctypes.c_double), ("t_ortho_ms", ctypes.c_double),
-                ("t_rr_ms", ctypes.c_double), ("filter_bytes", ctypes.c_double)]
+                ("t_rr_ms", ctypes.c_double), ("filter_bytes", ctypes.c_double),
+                ("jacobi_sweeps", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -94,7 +95,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_gemm_tn": (ctypes.c_int, [P, I64, I32, P, I64, I32, I64, D, I32, P, I64, P, SZ, P]),
         "scsf_gemm_nn": (ctypes.c_int, [P, I64, I64, I32, P, I64, I32, D, D, P, I64, P]),
         "scsf_chol_inv": (ctypes.c_int, [P, I64, I32, I64, P, P, SZ, P]),
-        "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, SZ, P]),
+        "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -355,12 +356,14 @@ def chol_inv(S: torch.Tensor, nrows: int = 1):
     return R
 
 
-def syev_small(G: torch.Tensor):
+def syev_small(G: torch.Tensor, return_sweeps: bool = False):
     """theta ascending, Z (column-major [b, b]) with G = Z diag(theta) Z^T (upper triangle of G used)."""
     lib = load_library()
     b = G.shape[0]
     ws = _workspace(lib.scsf_dev_workspace_bytes(1, b, b), G.device)
     theta = torch.empty(b, dtype=torch.float64, device=G.device)
     Z = torch.empty_like(G)
-    _check(lib.scsf_syev_small(_ptr(G), b, b, _ptr(theta), _ptr(Z), _ptr(ws), ws.numel(), _stream()))
-    return theta, Z
+    sw = ctypes.c_int32(0)
+    _check(lib.scsf_syev_small(_ptr(G), b, b, _ptr(theta), _ptr(Z), ctypes.byref(sw), _ptr(ws), ws.numel(),
+                               _stream()))
+    return (theta, Z, sw.value) if return_sweeps else (theta, Z)
