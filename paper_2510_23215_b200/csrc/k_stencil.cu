@@ -200,8 +200,10 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
       if (hzm) czm = ldg4_nc(cf + 3 * ldc + k0 - sxy);
     }
     const bool hm = k0 >= 1, hp = k0 + 4 < n;
-#pragma unroll 2
-    for (int j = j0; j < j1; ++j) {
+#pragma unroll
+    for (int jj = 0; jj < CB; ++jj) {
+      const int j = j0 + jj;
+      if (j >= j1) break;
       const double* __restrict__ x = X + (int64_t)j * ldv;
       const double4 xc = ldg4_nc(x + k0);
       const double xl = hm ? x[k0 - 1] : 0.0;
@@ -339,7 +341,7 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
                    ((uintptr_t)X % 32 == 0) && ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0) &&
                    (Xp == nullptr || (uintptr_t)Xp % 32 == 0);
   if (vec) {
-    constexpr int CB = 4;
+    constexpr int CB = 2;     // 2 columns per CTA: ~5x more CTAs than CB = 4, enough warps to hide latency
     dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
     if (ops->dim == 2)
       k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);

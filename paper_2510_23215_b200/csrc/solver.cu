@@ -122,14 +122,17 @@ int set_timing(int on) {
   return old;
 }
 
+static thread_local cudaEvent_t t_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
 struct PhaseTimer {
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t* ev = t_phase_ev;      // created once per host thread, reused by every operator
   bool on = false;
   double filter = 0, ortho = 0, rr = 0;
   int init() {
     on = g_timing != 0;
     if (!on) return SCSF_OK;
-    for (auto& e : ev) SCSF_CUDA_CHECK(cudaEventCreate(&e));
+    for (int i = 0; i < 4; ++i)
+      if (!ev[i]) SCSF_CUDA_CHECK(cudaEventCreate(&ev[i]));
     return SCSF_OK;
   }
   int mark(int i, cudaStream_t s) {
@@ -147,10 +150,6 @@ struct PhaseTimer {
     ortho += b;
     rr += c;
     return SCSF_OK;
-  }
-  ~PhaseTimer() {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
   }
 };
 
