@@ -63,6 +63,9 @@ int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double*
                   const double* c, double* coef, cudaStream_t s);
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
                  int ncols, const double* fp, int step, cudaStream_t s);
+bool filter_resident_ok(const scsf_ops* ops);
+int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
+                         const double* fp, int m, cudaStream_t s);
 
 }  // namespace scsf
 
@@ -188,6 +191,11 @@ int scsf_cheb_filter(const scsf_ops* ops, int32_t op_index, const double* Y0, in
   cudaStream_t s = (cudaStream_t)stream;
   double hfp[4] = {lambda, c, e, 0.0};
   SCSF_CUDA_CHECK(cudaMemcpyAsync(fp, hfp, sizeof(hfp), cudaMemcpyHostToDevice, s));
+  if (filter_resident_ok(ops) && !(getenv("SCSF_FILTER_STREAMING") && getenv("SCSF_FILTER_STREAMING")[0] == '1')) {
+    SCSF_TRY(filter_resident_impl(ops, op_index, Y0, Ym, ldy, k, fp, degree, s));
+    SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return SCSF_OK;
+  }
   // rotate over {Y0 (read-only), B1, B2, Ym}: Y_{s+1} never overwrites Y_s or Y_{s-1}
   const double* prev = nullptr;
   const double* cur = Y0;

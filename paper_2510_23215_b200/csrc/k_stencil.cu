@@ -266,6 +266,81 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
   }
 }
 
+// ------------------------------------------- column-resident filter (2-D) ----
+// All m steps of Alg. 1 for one column in one CTA (small grids, n <= RES_MAX_N):
+// Y_s double-buffered in shared memory, Y_{s-1} of the thread's own points in
+// registers, x-neighbours k +- 1 by warp shuffles (lanes hold consecutive k),
+// y-neighbours k +- nx from shared memory.  HBM traffic per filter: read Y_0,
+// write Y_m (16 n B per column) + the coefficient arrays (L2-resident, shared
+// by all columns).  Bound: shared-memory / L2 bandwidth, not HBM.
+constexpr int RES_T = 1024;
+constexpr int RES_PPT = 12;
+constexpr int RES_MAX_N = RES_T * RES_PPT;     // 12288 (smem 2 * 96 KB)
+
+__global__ void __launch_bounds__(RES_T, 1) k_filter_res2d(const double* __restrict__ cf, int64_t ldc, int nx,
+                                                           int n, const double* __restrict__ X, int64_t ldv,
+                                                           double* __restrict__ Out, const double* __restrict__ fp,
+                                                           int m) {
+  extern __shared__ double rbuf[];               // [2][n]
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const double* x0 = X + (int64_t)j * ldv;
+  double* out = Out + (int64_t)j * ldv;
+  const double lam = fp[0], c = fp[1], e = fp[2];
+  const double s1 = e / (lam - c);
+  double yprev[RES_PPT];
+#pragma unroll
+  for (int i = 0; i < RES_PPT; ++i) {
+    const int k = tid + RES_T * i;
+    yprev[i] = 0.0;
+    if (k < n) rbuf[k] = x0[k];
+  }
+  __syncthreads();
+  double sig = s1;
+  for (int st = 0; st < m; ++st) {
+    double a, bco;
+    if (st == 0) {
+      a = s1 / e;
+      bco = 0.0;
+    } else {                                     // same operation sequence as step_scalars()
+      const double sn = 1.0 / (2.0 / s1 - sig);
+      a = 2.0 * sn / e;
+      bco = -sn * sig;
+      sig = sn;
+    }
+    const double* cur = rbuf + (st & 1) * n;
+    double* nxt = rbuf + ((st + 1) & 1) * n;
+#pragma unroll
+    for (int i = 0; i < RES_PPT; ++i) {
+      const int k = tid + RES_T * i;
+      if (RES_T * i >= n) break;                 // uniform across the CTA
+      const bool in = k < n;
+      const double xc = in ? cur[k] : 0.0;
+      double xl = __shfl_up_sync(0xffffffffu, xc, 1);
+      double xr = __shfl_down_sync(0xffffffffu, xc, 1);
+      if (lane == 0) xl = (in && k >= 1) ? cur[k - 1] : 0.0;
+      if (lane == 31) xr = (k + 1 < n) ? cur[k + 1] : 0.0;
+      if (in) {
+        const double xd = (k >= nx) ? cur[k - nx] : 0.0;
+        const double xu = (k + nx < n) ? cur[k + nx] : 0.0;
+        const double cxm = (k >= 1) ? __ldg(cf + ldc + k - 1) : 0.0;
+        const double cym = (k >= nx) ? __ldg(cf + 2 * ldc + k - nx) : 0.0;
+        double v = (__ldg(cf + k) - c) * xc;
+        v = fma(__ldg(cf + ldc + k), xr, v);
+        v = fma(cxm, xl, v);
+        v = fma(__ldg(cf + 2 * ldc + k), xu, v);
+        v = fma(cym, xd, v);
+        v *= a;
+        if (st > 0) v = fma(bco, yprev[i], v);
+        yprev[i] = xc;
+        nxt[k] = v;
+      }
+    }
+    __syncthreads();
+  }
+  const double* fin = rbuf + (m & 1) * n;
+  for (int k = tid; k < (int)ldv; k += RES_T) out[k] = (k < n) ? fin[k] : 0.0;
+}
+
 // ---------------------------------------------------------- residuals ----
 // For active column j: res[j] = ||W_j - theta_j V_j||_2, wn[j] = ||W_j||_2 (fixed-order sums).
 __global__ void __launch_bounds__(512) k_resid(const double* __restrict__ V, const double* __restrict__ W,
@@ -327,6 +402,27 @@ int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaSt
   SCSF_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
   int blocks = min(ceil_div(n, 256), 148 * 4);
   k_gershgorin<<<blocks, 256, 0, s>>>(cf, ops->dim, ops->nx, ops->ny, n, ops->ld, out);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+static int g_res_attr = 0;
+bool filter_resident_ok(const scsf_ops* ops) {
+  return ops->dim == 2 && (int64_t)ops->nx * ops->ny <= RES_MAX_N;
+}
+
+// Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.
+int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
+                         const double* fp, int m, cudaStream_t s) {
+  if (ncols <= 0) return SCSF_OK;
+  const int n = ops->nx * ops->ny;
+  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  if (!g_res_attr) {
+    SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * RES_MAX_N * (int)sizeof(double)));
+    g_res_attr = 1;
+  }
+  k_filter_res2d<<<ncols, RES_T, (size_t)2 * n * sizeof(double), s>>>(cf, ops->ld, ops->nx, n, X, ldv, Out, fp, m);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

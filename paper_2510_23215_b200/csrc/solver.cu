@@ -22,6 +22,9 @@ namespace scsf {
 // kernels (k_*.cu)
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out,
                  int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s);
+bool filter_resident_ok(const scsf_ops* ops);
+int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
+                         const double* fp, int m, cudaStream_t s);
 int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
                const double* theta, double* res, double* wn, cudaStream_t s);
 int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s);
@@ -206,11 +209,17 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
     double* y[3] = {w.V + (int64_t)kL * w.ldv, w.T1 + (int64_t)kL * w.ldv, w.T2 + (int64_t)kL * w.ldv};
     // 1. Chebyshev filter (Alg. 1) on the active block
     SCSF_TRY(tm.mark(0, s));
-    SCSF_TRY(stencil_impl(ops, op, y[0], nullptr, y[1], w.ldv, ba, w.fp, 0, s));
-    for (int st_i = 1; st_i < degree; ++st_i)
-      SCSF_TRY(stencil_impl(ops, op, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], w.ldv, ba, w.fp,
-                            st_i, s));
-    double* F = y[degree % 3];
+    double* F;
+    if (filter_resident_ok(ops)) {
+      SCSF_TRY(filter_resident_impl(ops, op, y[0], y[1], w.ldv, ba, w.fp, degree, s));
+      F = y[1];
+    } else {
+      SCSF_TRY(stencil_impl(ops, op, y[0], nullptr, y[1], w.ldv, ba, w.fp, 0, s));
+      for (int st_i = 1; st_i < degree; ++st_i)
+        SCSF_TRY(stencil_impl(ops, op, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], w.ldv, ba, w.fp,
+                              st_i, s));
+      F = y[degree % 3];
+    }
     SCSF_TRY(tm.mark(1, s));
     // algorithmic bytes: first step reads Y0 + writes Y1, later steps read Y_s, Y_{s-1}
     // and write Y_{s+1}; one pass over the coefficient arrays per step

@@ -48,10 +48,17 @@ def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
 
 
 # -------------------------------------------------------------------- filter ----
+@pytest.mark.parametrize("streaming", [False, True])
 @pytest.mark.parametrize("cfg_name,nx,k,m", [("C1", 32, 20, 20), ("C3", 29, 9, 7), ("C4", 11, 13, 20),
-                                             ("C2", 40, 1, 1)])
-def test_filter_matches_oracle(lib, cfg_name, nx, k, m):
+                                             ("C2", 40, 1, 1), ("C2", 100, 6, 20), ("C5", 110, 3, 5)])
+def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
+    """Both filter kernels: column-resident (2-D, n <= 12288) and streaming (per-step launches,
+    vectorised when nx % 4 == 0, scalar otherwise); SCSF_FILTER_STREAMING=1 forces streaming."""
     import torch
+    if streaming:
+        monkeypatch.setenv("SCSF_FILTER_STREAMING", "1")
+    else:
+        monkeypatch.delenv("SCSF_FILTER_STREAMING", raising=False)
     cfg = synth.get_config(cfg_name).with_(nx=nx)
     f = synth.make_batch(cfg, 2)
     ops, _ = device_problem(f)
