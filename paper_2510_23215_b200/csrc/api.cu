@@ -40,6 +40,7 @@ int sort_impl(const double* params, int N, int dim, int p, int F, int p0, int st
               double* d2_best, double* d2_second, Arena& a, cudaStream_t s);
 // k_dense.cu / k_small.cu primitives
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
+size_t small_scratch_doubles(int b);
 int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, int b2, int64_t n,
             double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s);
 int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
@@ -368,6 +369,7 @@ size_t scsf_dev_workspace_bytes(int64_t n, int32_t b1, int32_t b2) {
   const int bm = b1 > b2 ? b1 : b2;
   a.take<double>((int64_t)tn_partial_doubles(n, b1, b2));
   a.take<double>(3 * (int64_t)bm * bm + 2);
+  a.take<double>((int64_t)small_scratch_doubles(bm));
   a.take<Ctrl>(1);
   return a.off;
 }
@@ -406,7 +408,7 @@ int scsf_chol_inv(const double* S, int64_t lds, int32_t b, int64_t nrows, double
                   void* stream) {
   SCSF_ARG_CHECK(S && Rinv && b >= 1 && b <= 384 && lds >= b, "bad chol_inv arguments");
   Arena a(ws, ws_bytes);
-  double* scratch = a.take<double>((int64_t)b * b);
+  double* scratch = a.take<double>((int64_t)small_scratch_doubles(b));
   Ctrl* ctrl = a.take<Ctrl>(1);
   if (a.overflow || !ws) {
     set_error("workspace too small");
@@ -430,7 +432,7 @@ int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, doub
                     size_t ws_bytes, void* stream) {
   SCSF_ARG_CHECK(G && theta && Z && b >= 1 && b <= 384 && ldg >= b, "bad syev_small arguments");
   Arena a(ws, ws_bytes);
-  double* g = a.take<double>((int64_t)b * b + 2);
+  double* g = a.take<double>((int64_t)small_scratch_doubles(b));
   double* zw = a.take<double>((int64_t)b * b);
   Ctrl* ctrl = a.take<Ctrl>(1);
   if (a.overflow || !ws) {

@@ -194,7 +194,7 @@ constexpr int V2_T = 64, V2_KC = 32, V2_P = V2_KC + 4;   // tile, k-chunk, pitch
 // ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
 __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
                                                   const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
-                                                  int64_t kchunk, int upper, double* __restrict__ P) {
+                                                  int64_t kchunk, int upper, int a16, double* __restrict__ P) {
   extern __shared__ __align__(16) double smd[];
   double* xs = smd;                                  // [2][64][36]
   double* ys = smd + 2 * V2_T * V2_P;                // [2][64][36]
@@ -219,8 +219,17 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
       double* dx = xs + (stage * V2_T + col) * V2_P + 2 * seg;
       double* dy = ys + (stage * V2_T + col) * V2_P + 2 * seg;
       const bool okx = (i0 + col < b1) && rem > 0, oky = (j0 + col < b2) && rem > 0;
-      cp_async16(dx, okx ? (const void*)(X + k + (int64_t)(i0 + col) * ldx) : (const void*)X, okx ? 8 * rem : 0);
-      cp_async16(dy, oky ? (const void*)(Y + k + (int64_t)(j0 + col) * ldy) : (const void*)Y, oky ? 8 * rem : 0);
+      const double* sx = okx ? X + k + (int64_t)(i0 + col) * ldx : X;
+      const double* sy = oky ? Y + k + (int64_t)(j0 + col) * ldy : Y;
+      if (a16) {
+        cp_async16(dx, sx, okx ? 8 * rem : 0);
+        cp_async16(dy, sy, oky ? 8 * rem : 0);
+      } else {                         // odd leading dimension: 8-byte copies
+        cp_async8(dx, sx, okx ? 8 : 0);
+        cp_async8(dx + 1, okx && rem > 1 ? sx + 1 : sx, (okx && rem > 1) ? 8 : 0);
+        cp_async8(dy, sy, oky ? 8 : 0);
+        cp_async8(dy + 1, oky && rem > 1 ? sy + 1 : sy, (oky && rem > 1) ? 8 : 0);
+      }
     }
   };
 
@@ -278,7 +287,7 @@ constexpr int NN2_MAX_K = 128;
 __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
                                                   const double* __restrict__ M, int64_t ldm, int b2,
                                                   double alpha, double beta, double* Out, int64_t ldo,
-                                                  int tri_upper) {
+                                                  int tri_upper, int a16) {
   extern __shared__ __align__(16) double smd[];
   const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
   double* xp = smd;                                  // [b1r][68]: xp[k*68 + r]
@@ -298,8 +307,14 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
       const int k = c * V2_KC + kk;
       const int rr = 2 * seg;
       const int rem = (k < b1) ? max(0, min(2, rows_here - rr)) : 0;
-      cp_async16(xp + k * (V2_T + 4) + rr, rem ? (const void*)(X + r0 + rr + (int64_t)k * ldx) : (const void*)X,
-                 8 * rem);
+      const double* src = rem ? X + r0 + rr + (int64_t)k * ldx : X;
+      double* dst = xp + k * (V2_T + 4) + rr;
+      if (a16) {
+        cp_async16(dst, src, 8 * rem);
+      } else {                         // odd leading dimension: 8-byte copies
+        cp_async8(dst, src, rem ? 8 : 0);
+        cp_async8(dst + 1, rem > 1 ? src + 1 : src, rem > 1 ? 8 : 0);
+      }
     }
   };
   auto issue_m = [&](int c, int j0, int stage) {   // 64 columns x 32 k (8-byte copies; ldm may be odd)
@@ -431,7 +446,8 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
-  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, P);
+  const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
+  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P);
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b1, 32), b2);
   k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper, C, ldc);
@@ -449,7 +465,9 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
   }
   SCSF_TRY(dense_init_attrs());
   if (b1 <= NN2_MAX_K) {
-    k_gemm_nn2<<<ceil_div(n, V2_T), 256, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri);
+    const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
+    k_gemm_nn2<<<ceil_div(n, V2_T), 256, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
+                                                            a16);
   } else {
     int b1r = (max(b1, 1) + 3) & ~3;
     size_t smem = (size_t)b1r * NN_LDS * sizeof(double);

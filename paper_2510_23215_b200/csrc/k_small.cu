@@ -20,79 +20,112 @@
 namespace scsf {
 
 // ------------------------------------------------------------- chol_inv ----
-// Cholesky with the inverse factor built in the same elimination sweep
-// (Gauss-Jordan on [S | I]): at step j, row j of R = A[j, j:] / r_jj and the
-// trailing block is updated; the same row operations applied to I give
-// B = L^{-1} = (R^{-1})^T.  Storage: A (b x b, col-major, ld b): upper triangle
-// holds A / R, strict lower triangle holds B (B[i][c] at A[i + c b], c < i);
-// binv[i] = B[i][i].  1024 threads as 32 x 32 (tx = lane, ty = warp): every
-// loop is a strided 2-D loop, no runtime integer division.
-template <bool SMEM>
-__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S, int64_t lds, int b,
-                                                   int64_t nrows, double* __restrict__ Rinv,
-                                                   double* __restrict__ gA, Ctrl* ctrl) {
-  extern __shared__ double sm[];
-  double* A = SMEM ? sm : gA;
-  __shared__ double binv[384];
-  __shared__ double rj[384], bj[384];   // row j of R and of B, contiguous (no bank conflicts)
+// Cholesky S = R^T R with the inverse factor built in the same elimination
+// sweep (Gauss-Jordan on [S | I]): at step j, row j of R = A[j, j:] / r_jj and
+// the trailing block is updated; the same row operations applied to I give
+// B = R^{-T} (lower).  Register-resident for b <= 32*NS: thread (warp w, lane
+// l) owns M[i][k], i = w + 32 s, k = l + 32 q (s, q < NS); the upper triangle
+// of M holds A / R, the strict lower triangle B, binv[] the diagonal of B.
+// One __syncthreads per step: the owner warp of row j broadcasts the scaled
+// row through a double-buffered shared row, every thread then applies the
+// rank-1 update  M[i][k] -= row[i] row[k]  for i > j and (k >= i or k <= j)
+// (trailing Schur complement and the rows of B below j alike).
+// Tsub (optional): factor S - Tsub instead of S (blocked Schur complement).
+template <int NS>
+__device__ __forceinline__ double sel(const double (&a)[NS][NS], int s, int q) {
+  double v = 0.0;
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+#pragma unroll
+    for (int y = 0; y < NS; ++y)
+      if (x == s && y == q) v = a[x][y];
+  return v;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(1024, 1) k_chol_reg(const double* __restrict__ S, int64_t lds,
+                                                      const double* __restrict__ Tsub, int64_t ldt, int b,
+                                                      int64_t nrows, double* __restrict__ Rinv, int64_t ldr,
+                                                      Ctrl* ctrl) {
+  __shared__ double rowbuf[2][32 * NS];
+  __shared__ double binv[32 * NS];
+  __shared__ double sdiag[32 * NS];
   __shared__ int fail;
   __shared__ double shift;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
+  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5;
+  double a[NS][NS];
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (tid == 0) {
       fail = 0;
       shift = 0.0;
       if (attempt == 1) {
         double tr = 0.0;
-        for (int i = 0; i < b; ++i) tr += fabs(S[i + i * lds]);
+        for (int i = 0; i < b; ++i) tr += fabs(S[i + i * lds] - (Tsub ? Tsub[i + i * ldt] : 0.0));
         shift = 11.0 * ((double)nrows * b + (double)b * (b + 1)) * 1.1102230246251565e-16 * tr;
       }
     }
+    if (tid < 32 * NS) binv[tid] = 1.0;
     __syncthreads();
-    // load: symmetrised upper triangle (+ shift on the diagonal), zero lower triangle
-    for (int k = ty; k < b; k += 32)
-      for (int i = tx; i < b; i += 32) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const int i = w + 32 * s, k = l + 32 * q;
         double v = 0.0;
-        if (i < k) v = S[i + k * lds];                 // Gram: upper triangle is the valid half
-        else if (i == k) v = S[i + i * lds] + shift;
-        A[i + k * b] = v;
+        if (i <= k && k < b) {
+          v = S[i + k * lds];
+          if (Tsub) v -= Tsub[i + k * ldt];
+          if (i == k) {
+            if (attempt == 0) sdiag[i] = v;
+            v += shift;
+          }
+        }
+        a[s][q] = v;
       }
-    for (int i = tid; i < b; i += 1024) binv[i] = 1.0;
     __syncthreads();
     for (int j = 0; j < b; ++j) {
-      const double d = A[j + j * b];
-      const double bj_old = binv[j];
-      if (!(d > 1e-14 * fabs(S[j + (int64_t)j * lds])) || !isfinite(d)) {
-        if (tid == 0) fail = 1;
+      const int sj = j >> 5, lj = j & 31;
+      double* rb = rowbuf[j & 1];
+      if (w == lj) {                                   // owner warp of row j
+        const double d = __shfl_sync(0xffffffffu, sel<NS>(a, sj, sj), lj);
+        const bool bad = !(d > 1e-14 * fabs(sdiag[j])) || !isfinite(d);
+        const double r = sqrt(d), rinv = 1.0 / r;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const int k = l + 32 * q;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            if (s != sj) continue;
+            double v = a[s][q];
+            if (k == j) {
+              a[s][q] = r;
+              const double bjj = binv[j] * rinv;
+              binv[j] = bjj;
+              rb[j] = bjj;
+            } else if (k < b) {
+              v *= rinv;
+              a[s][q] = v;
+              rb[k] = v;
+            }
+          }
+        }
+        if (bad && l == 0) fail = 1;
       }
-      __syncthreads();                       // every thread has read d and bj_old
+      __syncthreads();
       if (fail) break;
-      const double r = sqrt(d), rinv = 1.0 / r;
-      const double bjj = bj_old * rinv;      // B[j][j] after scaling
-      // phase 1: row j of R and row j of B scaled by 1/r_jj (B row kept in A for the output)
-      for (int k = j + 1 + tid; k < b; k += 1024) rj[k] = A[j + k * b] * rinv;
-      for (int c = tid; c < j; c += 1024) {
-        const double v = A[j + c * b] * rinv;
-        bj[c] = v;
-        A[j + c * b] = v;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int i = w + 32 * s;
+        if (i <= j || i >= b) continue;
+        const double ri = rb[i];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const int k = l + 32 * q;
+          if (k < b && (k >= i || k <= j)) a[s][q] = fma(-ri, rb[k], a[s][q]);
+        }
       }
-      if (tid == 0) {
-        A[j + j * b] = r;
-        binv[j] = bjj;
-        bj[j] = bjj;
-      }
-      __syncthreads();
-      // phase 2: trailing update (upper, j < i <= k) and B rows i > j
-      for (int k = j + 1 + ty; k < b; k += 32) {
-        const double rjk = rj[k];
-        for (int i = j + 1 + tx; i <= k; i += 32) A[i + k * b] -= rj[i] * rjk;
-      }
-      for (int c = ty; c <= j; c += 32) {
-        const double bjc = bj[c];
-        for (int i = j + 1 + tx; i < b; i += 32) A[i + c * b] -= rj[i] * bjc;
-      }
-      __syncthreads();
     }
+    __syncthreads();
     if (!fail) break;
     if (tid == 0 && ctrl) {
       ctrl->chol_fail = 1;
@@ -100,13 +133,13 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S,
     }
     __syncthreads();
   }
-  // R^{-1}[i][c] = B[c][i] (upper)
-  for (int c = ty; c < b; c += 32)
-    for (int i = tx; i < b; i += 32) {
-      double v = 0.0;
-      if (i == c) v = binv[i];
-      else if (i < c) v = A[c + i * b];
-      Rinv[i + c * b] = v;
+  // R^{-1}[k][i] = B[i][k] (i > k), diagonal binv, zero below the diagonal
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const int i = w + 32 * s, k = l + 32 * q;
+      if (i < b && k < b) Rinv[k + (int64_t)i * ldr] = (i > k) ? a[s][q] : (i == k ? binv[i] : 0.0);
     }
 }
 
@@ -472,6 +505,251 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_x(const double* __restrict__
     }
 }
 
+// ------------------------------------------------ jacobi_eig (G | Z split) ----
+// The same two-sided cyclic Jacobi with the XOR ("hypercube") ordering, split
+// in two kernels so the rotation accumulator no longer competes with G for the
+// SM.  k_jacobi_g (one CTA) rotates G only (upper triangle in shared memory)
+// and records every round that rotated anything: the round index m and the
+// (c, s) of its B/2 pairs (pair slot = lo with bit h removed).  k_jacobi_z
+// (B/16 CTAs, 16 rows of Z each) then replays the record on Z = I row-slice by
+// row-slice (rows of Z transform independently under Z <- Z J) and writes the
+// eigenvector columns in ascending-eigenvalue order.
+constexpr int JREC_SWEEPS = 24;                  // recorded sweeps (>= the sweep cap)
+
+__device__ __forceinline__ int ins0(int a, int h) {    // insert a 0 bit at position h
+  const int lowmask = (1 << h) - 1;
+  return ((a & ~lowmask) << 1) | (a & lowmask);
+}
+
+// Newton-refined fp64 reciprocal / reciprocal square root for normal, finite
+// arguments: MUFU seed + two Newton steps (no slow-path subroutine calls on
+// the round's critical path).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
+template <int LOGB>
+__global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__ Gin, int64_t ldg, int b,
+                                                      double2* __restrict__ rec, int* __restrict__ recm,
+                                                      int* __restrict__ nrec_out, double* __restrict__ theta_out,
+                                                      int* __restrict__ rank_out, int max_sweeps, Ctrl* ctrl) {
+  constexpr int B = 1 << LOGB;
+  constexpr int GP = B + 1;
+  constexpr int H2 = B / 2;
+  extern __shared__ double G[];                     // [B][GP], upper triangle used
+  __shared__ __align__(16) double2 cs_cs[B];        // (c, s) of the pair whose lower index is lo; s == 0: no rotation
+  __shared__ double cs_t[B];
+  __shared__ double red[32];
+  __shared__ double floor_s;
+  __shared__ int any_rot[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = 1e-14, tol2 = tol * tol;
+
+  double dmax = 0.0;
+  for (int idx = tid; idx < B * B; idx += 1024) {
+    const int i = idx >> LOGB, j = idx & (B - 1);
+    if (i <= j) {
+      const double v = (i < b && j < b) ? Gin[i + (int64_t)j * ldg] : 0.0;
+      G[i * GP + j] = v;
+      if (i == j) dmax = fmax(dmax, fabs(v));
+    }
+  }
+  dmax = warp_max(dmax);
+  if (lane == 0) red[warp] = dmax;
+  if (tid < 2) any_rot[tid] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+    floor_s = 4.0 * 2.220446049250313e-16 * v;
+  }
+  __syncthreads();
+  const double gfloor = floor_s;
+  int nrec = 0;                                     // uniform across the CTA
+  int sweep = 0;
+  for (; sweep <= max_sweeps; ++sweep) {
+    double mx = 0.0;
+    for (int i = warp; i < b; i += 32)
+      for (int j = i + 1 + lane; j < b; j += 32) {
+        const double g = fabs(G[i * GP + j]);
+        if (g > gfloor) mx = fmax(mx, g / fmax(sqrt(fabs(G[i * GP + i] * G[j * GP + j])), 1e-300));
+      }
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+      red[0] = v;
+    }
+    __syncthreads();
+    const bool done = red[0] <= tol;
+    __syncthreads();
+    if (done || sweep == max_sweeps || sweep >= JREC_SWEEPS) break;
+    for (int m = 1; m < B; ++m) {
+      const int h = 31 - __clz(m);
+      const int par = m & 1;
+      // ---- rotation of pair (lo, lo ^ m): t = sgn(d) e / (|d| + sqrt(d^2 + e^2)), d = g_qq - g_pp, e = 2 g_pq
+      if (tid < H2) {
+        const int lo = ins0(tid, h), hi = lo ^ m;
+        double c = 1.0, sn = 0.0, t = 0.0;
+        if (hi < b) {
+          const double gpq = G[lo * GP + hi], gpp = G[lo * GP + lo], gqq = G[hi * GP + hi];
+          if (gpq * gpq > tol2 * fabs(gpp * gqq) && fabs(gpq) > gfloor) {
+            const double d = gqq - gpp, e2 = 2.0 * gpq;
+            const double q = fma(d, d, e2 * e2);
+            const double r = q * rsqrt_nr(q);
+            t = copysign(1.0, d) * e2 * rcp_nr(fabs(d) + r);
+            c = rsqrt_nr(fma(t, t, 1.0));
+            sn = t * c;
+            any_rot[par] = 1;
+          }
+        }
+        cs_cs[lo] = make_double2(c, sn);
+        cs_t[lo] = t;
+        rec[(int64_t)nrec * H2 + tid] = make_double2(c, sn);
+      }
+      if (tid == 0) any_rot[par ^ 1] = 0;
+      __syncthreads();
+      if (!any_rot[par]) continue;                  // uniform: the record slot is reused
+      if (tid == 0) recm[nrec] = m;
+      ++nrec;
+      // ---- G <- J^T G J on blocks {ilo, ihi} x {jlo, jhi}, ilo <= jlo (upper storage)
+      for (int ai = warp; ai < H2; ai += 32) {
+        const int ilo = ins0(ai, h);
+        const int ihi = ilo ^ m;
+        const double2 cs1 = cs_cs[ilo];
+        for (int aj = ai + lane; aj < H2; aj += 32) {
+          const int jlo = ins0(aj, h);
+          const double2 cs2 = cs_cs[jlo];
+          if (cs1.y == 0.0 && cs2.y == 0.0) continue;
+          const int jhi = jlo ^ m;
+          if (ilo == jlo) {
+            const int ipq = ilo * GP + ihi;
+            const double gpq = G[ipq], t = cs_t[ilo];
+            G[ilo * GP + ilo] -= t * gpq;
+            G[ihi * GP + ihi] += t * gpq;
+            G[ipq] = 0.0;
+            continue;
+          }
+          const int ia = ilo * GP + jlo;
+          const int ib = ilo * GP + jhi;
+          const int ic = min(ihi, jlo) * GP + max(ihi, jlo);
+          const int id = min(ihi, jhi) * GP + max(ihi, jhi);
+          const double a = G[ia], bb = G[ib], cc = G[ic], d = G[id];
+          const double c1 = cs1.x, s1 = cs1.y, c2 = cs2.x, s2 = cs2.y;
+          const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;
+          const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
+          G[ia] = c1 * a2 - s1 * c2v;
+          G[ib] = c1 * b2 - s1 * d2;
+          G[ic] = s1 * a2 + c1 * c2v;
+          G[id] = s1 * b2 + c1 * d2;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    *nrec_out = nrec;
+    if (ctrl) {
+      if (sweep >= max_sweeps || sweep >= JREC_SWEEPS) ctrl->nonfinite |= 2;
+      ctrl->pad[0] += sweep;
+    }
+  }
+  if (tid < b) {
+    const double v = G[tid * GP + tid];
+    int rk = 0;
+    for (int j = 0; j < b; ++j) {
+      const double w = G[j * GP + j];
+      rk += (w < v) || (w == v && j < tid);
+    }
+    rank_out[tid] = rk;
+    theta_out[rk] = v;
+  }
+}
+
+// Replay of the recorded rounds on Z = I: CTA z owns rows [16 z, 16 z + 16).
+// The record streams through shared memory in chunks of ZCH rounds (cp.async,
+// double-buffered), so the per-round work never waits on L2.
+constexpr int ZCH = 12;
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem) : "memory");
+}
+
+template <int LOGB>
+__global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restrict__ rec, const int* __restrict__ recm,
+                                                        const int* __restrict__ nrec_p, const int* __restrict__ rank,
+                                                        int b, double* __restrict__ Zout) {
+  constexpr int B = 1 << LOGB;
+  constexpr int H2 = B / 2;
+  constexpr int R = 16;
+  constexpr int ZP = B + 1;
+  constexpr int NT = H2 * R;
+  __shared__ double z[R * ZP];
+  __shared__ __align__(16) double2 rs[2][ZCH * H2];
+  __shared__ int ms[2][ZCH];
+  const int tid = threadIdx.x;
+  const int pslot = tid % H2, row = tid / H2;
+  const int x0 = blockIdx.x * R;
+  for (int i = tid; i < R * B; i += NT) {
+    const int r = i / B, cidx = i % B;
+    z[r * ZP + cidx] = (x0 + r == cidx) ? 1.0 : 0.0;
+  }
+  const int nrec = *nrec_p;
+  const int nch = (nrec + ZCH - 1) / ZCH;
+  auto load_chunk = [&](int ch, int buf) {
+    const int r0 = ch * ZCH, cnt = min(ZCH, nrec - r0);
+    for (int i = tid; i < cnt * H2; i += NT) cpa16(&rs[buf][i], rec + (int64_t)r0 * H2 + i);
+    if (tid < cnt) ms[buf][tid] = recm[r0 + tid];
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (nch > 0) load_chunk(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) {
+      load_chunk(ch + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int cnt = min(ZCH, nrec - ch * ZCH);
+    for (int k = 0; k < cnt; ++k) {
+      const double2 cs = rs[buf][k * H2 + pslot];
+      if (cs.y != 0.0) {
+        const int m = ms[buf][k];
+        const int h = 31 - __clz(m);
+        const int lo = ins0(pslot, h), hi = lo ^ m;
+        double* zr = z + row * ZP;
+        const double zl = zr[lo], zh = zr[hi];
+        zr[lo] = cs.x * zl - cs.y * zh;
+        zr[hi] = cs.y * zl + cs.x * zh;
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < R * B; i += NT) {
+    const int r = i / B, cidx = i % B;
+    const int x = x0 + r;
+    if (x < b && cidx < b) Zout[x + (int64_t)rank[cidx] * b] = z[r * ZP + cidx];
+  }
+}
+
 // ----------------------------------------------------------------- lock ----
 // theta/res/wn/rel are indexed by block column (0..b-1); active columns [kL, b).
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
@@ -607,24 +885,104 @@ __global__ void __launch_bounds__(256) k_gather_sign(const double* __restrict__ 
   for (int64_t k = threadIdx.x; k < n; k += blockDim.x) o[k] = sgn * v[k];
 }
 
+// Out (upper triangle) = A - B (upper triangles), b x b; zero block (rows x cols).
+__global__ void k_sub_upper(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
+                            int b, double* __restrict__ Out, int64_t ldo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (i <= k && k < b) Out[i + k * ldo] = A[i + k * lda] - B[i + k * ldb];
+}
+__global__ void k_zero_block(double* __restrict__ P, int64_t ld, int rows, int cols) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (i < rows && k < cols) P[i + k * ld] = 0.0;
+}
+
 // ------------------------------------------------------------------ host ----
 static int g_small_attr = 0;
 
-constexpr int CHOL_SMEM_MAX_B = 156;    // b*b*8 <= ~195 KB
 constexpr int JAC_SMEM_MAX_B = 133;     // (b(b+1)/2 + b*b)*8 <= ~213 KB
 
 static size_t jac_smem(int b) { return (size_t)((((b * (b + 1)) >> 1) + 1) & ~1) * 8 + (size_t)b * b * 8; }
 
 int set_small_attrs() {
   if (g_small_attr) return SCSF_OK;
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       CHOL_SMEM_MAX_B * CHOL_SMEM_MAX_B * 8));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)jac_smem(JAC_SMEM_MAX_B)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_x<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        128 * 129 * (int)sizeof(double)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_g<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       128 * 129 * (int)sizeof(double)));
   g_small_attr = 1;
   return SCSF_OK;
+}
+
+static int sub_upper_impl(const double* A, int64_t lda, const double* B, int64_t ldb, int b, double* Out,
+                          int64_t ldo, cudaStream_t s) {
+  k_sub_upper<<<dim3(ceil_div(b, 128), b), 128, 0, s>>>(A, lda, B, ldb, b, Out, ldo);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+static int zero_block_impl(double* P, int64_t ld, int rows, int cols, cudaStream_t s) {
+  k_zero_block<<<dim3(ceil_div(rows, 128), cols), 128, 0, s>>>(P, ld, rows, cols);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+// dense tiles (k_dense.cu)
+int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, int b2, int64_t n,
+            double alpha, int sym, double* C, int64_t ldc, double* P, cudaStream_t s);
+int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
+               double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s);
+
+static int chol_reg_launch(const double* S, int64_t lds, const double* T, int64_t ldt, int b, int64_t nrows,
+                           double* Rinv, int64_t ldr, Ctrl* ctrl, cudaStream_t s) {
+  if (b <= 32) k_chol_reg<1><<<1, 1024, 0, s>>>(S, lds, T, ldt, b, nrows, Rinv, ldr, ctrl);
+  else if (b <= 64) k_chol_reg<2><<<1, 1024, 0, s>>>(S, lds, T, ldt, b, nrows, Rinv, ldr, ctrl);
+  else if (b <= 96) k_chol_reg<3><<<1, 1024, 0, s>>>(S, lds, T, ldt, b, nrows, Rinv, ldr, ctrl);
+  else k_chol_reg<4><<<1, 1024, 0, s>>>(S, lds, T, ldt, b, nrows, Rinv, ldr, ctrl);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+// Blocked recursion for b > 128 (S = [S11 S12; . S22], b1 = 128):
+//   R11^{-1} = chol_inv(S11);  R12 = R11^{-T} S12;  R22^{-1} = chol_inv(S22 - R12^T R12);
+//   R^{-1} = [R11^{-1}, -R11^{-1} R12 R22^{-1}; 0, R22^{-1}]
+// scratch: >= small_scratch_doubles(b).  Every step runs in this library's kernels.
+static int chol_rec(const double* S, int64_t lds, const double* T, int64_t ldt, int b, int64_t nrows,
+                    double* Rinv, int64_t ldr, double* scratch, Ctrl* ctrl, cudaStream_t s) {
+  if (b <= 128) return chol_reg_launch(S, lds, T, ldt, b, nrows, Rinv, ldr, ctrl, s);
+  if (T) {
+    set_error("chol_inv: nested Schur complement");
+    return SCSF_ERR_NOT_IMPLEMENTED;
+  }
+  const int b1 = 128, b2 = b - b1;
+  double* R12 = scratch;                         // b1 x b2, ld b1
+  double* T22 = R12 + (int64_t)b1 * b2;          // b2 x b2, ld b2 (upper)
+  double* T2 = T22 + (int64_t)b2 * b2;           // b1 x b2, ld b1
+  double* P = T2 + (int64_t)b1 * b2;             // split-K partials (one split: n = b1 <= 128)
+  double* sub = P + (int64_t)b2 * b2 + (int64_t)b1 * b2;
+  SCSF_TRY(chol_reg_launch(S, lds, nullptr, 0, b1, nrows, Rinv, ldr, ctrl, s));
+  SCSF_TRY(gemm_tn(Rinv, ldr, b1, S + b1 * lds, lds, b2, b1, 1.0, 0, R12, b1, P, s));
+  SCSF_TRY(gemm_tn(R12, b1, b2, R12, b1, b2, b1, 1.0, 1, T22, b2, P, s));
+  double* Rinv22 = Rinv + b1 + (int64_t)b1 * ldr;
+  if (b2 <= 128) {
+    SCSF_TRY(chol_reg_launch(S + b1 + (int64_t)b1 * lds, lds, T22, b2, b2, nrows, Rinv22, ldr, ctrl, s));
+  } else {
+    // S22 - T22 materialised (upper triangle), then recurse
+    SCSF_TRY(sub_upper_impl(S + b1 + (int64_t)b1 * lds, lds, T22, b2, b2, sub, b2, s));
+    SCSF_TRY(chol_rec(sub, b2, nullptr, 0, b2, nrows, Rinv22, ldr, sub + (int64_t)b2 * b2, ctrl, s));
+  }
+  SCSF_TRY(gemm_nn_ex(R12, b1, b1, b2, Rinv22, ldr, b2, 1.0, 0.0, T2, b1, 1, s));
+  SCSF_TRY(gemm_nn_ex(Rinv, ldr, b1, b1, T2, b1, b2, -1.0, 0.0, Rinv + (int64_t)b1 * ldr, ldr, 0, s));
+  SCSF_TRY(zero_block_impl(Rinv + b1, ldr, b2, b1, s));    // strictly lower block
+  return SCSF_OK;
+}
+
+size_t small_scratch_doubles(int b) {
+  // chol_rec: per level 3 b1 b2 + 2 b2^2 (+ the materialised S22 - T22 and its own level);
+  // jacobi (b <= 128): the rotation record (JREC_SWEEPS x 127 rounds x 64 pairs of (c, s)) + indices
+  const size_t chol = (size_t)8 * b * b + 4096;
+  const size_t jac = (size_t)JREC_SWEEPS * 128 * 64 * 2 + (size_t)JREC_SWEEPS * 128 + 1024;
+  return chol > jac ? chol : jac;
 }
 
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
@@ -634,15 +992,25 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(set_small_attrs());
-  if (b <= CHOL_SMEM_MAX_B)
-    k_chol_inv<true><<<1, 1024, (size_t)b * b * sizeof(double), s>>>(S, lds, b, nrows, Rinv, scratch, ctrl);
-  else
-    k_chol_inv<false><<<1, 1024, 0, s>>>(S, lds, b, nrows, Rinv, scratch, ctrl);
+  return chol_rec(S, lds, nullptr, 0, b, nrows, Rinv, b, scratch, ctrl, s);
+}
+
+template <int LOGB>
+static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scratch, double* theta, double* Zout,
+                               Ctrl* ctrl, cudaStream_t s) {
+  constexpr int B = 1 << LOGB;
+  double2* rec = reinterpret_cast<double2*>(scratch);
+  int* recm = reinterpret_cast<int*>(scratch + (size_t)JREC_SWEEPS * 128 * 64 * 2);
+  int* nrec = recm + JREC_SWEEPS * 128;
+  int* rank = nrec + 32;
+  k_jacobi_g<LOGB><<<1, 1024, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank, 40, ctrl);
+  SCSF_LAUNCH_CHECK();
+  k_jacobi_z<LOGB><<<ceil_div(b, 16), 8 * B, 0, s>>>(rec, recm, nrec, rank, b, Zout);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
 
-// scratchG: >= b(b+1)/2 + 1 doubles; Z: b*b doubles (global fallback only)
+// scratchG: >= small_scratch_doubles(b) doubles; Z: b*b doubles (global fallback only)
 int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
                 double* Zout, Ctrl* ctrl, cudaStream_t s) {
   if (b > 384) {
@@ -650,13 +1018,10 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(set_small_attrs());
-  if (b <= 32)
-    k_jacobi_x<5><<<1, 1024, 32 * 33 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
-  else if (b <= 64)
-    k_jacobi_x<6><<<1, 1024, 64 * 65 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
-  else if (b <= 128)
-    k_jacobi_x<7><<<1, 1024, 128 * 129 * sizeof(double), s>>>(G, ldg, b, theta, Zout, 40, ctrl);
-  else if (b <= JAC_SMEM_MAX_B)
+  if (b <= 32) return jacobi_split_launch<5>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
+  if (b <= 64) return jacobi_split_launch<6>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
+  if (b <= 128) return jacobi_split_launch<7>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
+  if (b <= JAC_SMEM_MAX_B)
     k_jacobi<true><<<1, 1024, jac_smem(b), s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);
   else
     k_jacobi<false><<<1, 1024, 0, s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);

@@ -35,6 +35,7 @@ int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, in
 int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
                double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s);
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
+size_t small_scratch_doubles(int b);
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
                   Ctrl* ctrl, cudaStream_t s);
 int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
@@ -60,7 +61,7 @@ static void carve(Arena& a, SolveWS& w, int64_t n, int b) {
   w.Rinv = a.take<double>(bb);
   w.Zs = a.take<double>(bb);
   w.Zwork = a.take<double>(bb);
-  w.Gwork = a.take<double>(bb);
+  w.Gwork = a.take<double>((int64_t)small_scratch_doubles(b));
   w.C = a.take<double>(bb);
   w.P = a.take<double>((int64_t)tn_partial_doubles(n, b, b));
   w.theta = a.take<double>(b);
