@@ -211,6 +211,65 @@ int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* 
                       int32_t max_iter, uint64_t seed, double* evals, double* evecs, int64_t ld_vec,
                       scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------- row-partitioned solve ---- */
+/*
+ * One operator too large for one GPU's share of the work (BASELINE.json
+ * configs[4]): the grid rows of a 2-D operator are
+ * split into contiguous slabs, one per rank; every n x b block of Alg. 3
+ * holds only the rank's rows.  The exchange steps:
+ *  - before every stencil application (filter step, Alg. 1; W = AQ,
+ *    P:302): the slab's first / last grid row of every column goes to the
+ *    lower / upper neighbour (halo);
+ *  - every Gram / projection block X^T Y (CholQR l. 4 P:301, BCGS against the
+ *    locked vectors, G = Q^T A Q l. 5 P:302) and the residual norms (l. 7,
+ *    P:304, metric P:844) are summed over ranks;
+ *  - the b x b factorisation / eigensolve (ll. 4-6) runs replicated on every
+ *    rank on the identical all-reduced input, so every rank takes the same
+ *    locking decision;
+ *  - the sign convention of the returned vectors uses the global largest |.|
+ *    entry (all-gather of per-rank candidates).
+ * Operator arrays stay global (replicated: 8 (1 + dim) n bytes per operator,
+ * small next to the b-column blocks); the chain-head random block is the
+ * same global block on any partition (counter-based, global row index).
+ *
+ * scsf_comm: NCCL over NVLink/NVSwitch (one process per GPU; libnccl is
+ * resolved at run time from the process, i.e. the copy torch loaded) or an
+ * in-process loopback of `world` virtual ranks on one device (each driven
+ * by its own host thread; collectives meet at a host barrier, no kernel
+ * waits on another rank).  The loopback allocates its own tiny device
+ * scratch (pointer tables), the one exception to "the library never
+ * allocates device memory".
+ *
+ * scsf_comm_unique_id   128 B NCCL id (rank 0; the caller broadcasts it)
+ * scsf_comm_create      NCCL communicator for (rank, world); collective over
+ *                       all ranks (ncclCommInitRank)
+ * scsf_comm_create_loopback  out[world]: communicators of `world` virtual ranks
+ * scsf_slab_rows        rows [y0, y1) of `rank`: y0 = floor(rank ny / world)
+ * scsf_solve_queue_dist scsf_solve_queue on this rank's slab.  ops: the global
+ *                       operator batch (dim 2, nx % 4 == 0); [y0, y1) must be
+ *                       scsf_slab_rows(ny, world, rank).  evals dev
+ *                       [n_chain][L] (identical on every rank); evecs_local
+ *                       dev [n_chain][L][ld_vec] or NULL, the slab's rows
+ *                       (ld_vec >= nx (y1 - y0)).  Every rank must call it
+ *                       with the same chain and parameters.
+ * Errors as scsf_solve_queue; SCSF_ERR_NOT_IMPLEMENTED when NCCL cannot be
+ * loaded; SCSF_ERR_ARG for dim 3, nx % 4 != 0 or a slab that does not match.
+ */
+typedef struct scsf_comm scsf_comm;
+int scsf_comm_unique_id(void* id128);
+int scsf_comm_create(int32_t rank, int32_t world, const void* id128, scsf_comm** out);
+int scsf_comm_create_loopback(int32_t world, scsf_comm** out);
+int scsf_comm_destroy(scsf_comm* comm);
+int scsf_comm_rank(const scsf_comm* comm, int32_t* rank, int32_t* world);
+void scsf_slab_rows(int32_t ny, int32_t world, int32_t rank, int32_t* y0, int32_t* y1);
+size_t scsf_solve_dist_workspace_bytes(const scsf_ops* ops, int32_t y0, int32_t y1, int32_t L,
+                                       int32_t nex, int32_t world);
+int scsf_solve_queue_dist(const scsf_ops* ops, int32_t y0, int32_t y1, const int32_t* chain,
+                          int32_t n_chain, int32_t L, int32_t nex, int32_t degree, double tol,
+                          int32_t max_iter, uint64_t seed, double* evals, double* evecs_local,
+                          int64_t ld_vec, scsf_stats* st, scsf_comm* comm, void* ws,
+                          size_t ws_bytes, void* stream);
+
 /* ------------------------------------------- component entry points ---- */
 /*
  * Single steps of Alg. 3 exposed for parity tests and microbenchmarks.  Same

@@ -71,6 +71,7 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
 }  // namespace scsf
 
 #include "solver.cuh"
+#include "comm.cuh"
 
 using namespace scsf;
 
@@ -269,9 +270,10 @@ static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
                                     cudaMemcpyDeviceToDevice, s));
     if (evecs)
       SCSF_CUDA_CHECK(cudaMemcpy2DAsync(evecs + (int64_t)k * L * ld_vec, ld_vec * sizeof(double), w.V,
-                                        w.ldv * sizeof(double), n * sizeof(double), L, cudaMemcpyDeviceToDevice,
+                                        w.ldv * sizeof(double), w.n * sizeof(double), L, cudaMemcpyDeviceToDevice,
                                         s));
   }
+  (void)n;
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
   return worst;
 }
@@ -452,6 +454,100 @@ int scsf_syev_small(const double* G, int64_t ldg, int32_t b, double* theta, doub
     return SCSF_ERR_NUMERICAL;
   }
   return SCSF_OK;
+}
+
+
+/* ---------------------------------------------- row-partitioned solve ---- */
+struct scsf_comm;   // opaque: a scsf::Comm
+
+int scsf_comm_unique_id(void* id128) {
+  SCSF_ARG_CHECK(id128 != nullptr, "id128 is NULL");
+  return comm_unique_id(id128);
+}
+
+int scsf_comm_create(int32_t rank, int32_t world, const void* id128, scsf_comm** out) {
+  SCSF_ARG_CHECK(out && id128, "NULL argument");
+  SCSF_ARG_CHECK(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+  Comm* c = nullptr;
+  SCSF_TRY(comm_create_nccl(rank, world, id128, &c));
+  *out = reinterpret_cast<scsf_comm*>(c);
+  return SCSF_OK;
+}
+
+int scsf_comm_create_loopback(int32_t world, scsf_comm** out) {
+  SCSF_ARG_CHECK(out && world >= 1, "bad loopback arguments");
+  std::vector<Comm*> cs(world, nullptr);
+  SCSF_TRY(comm_create_loopback(world, cs.data()));
+  for (int r = 0; r < world; ++r) out[r] = reinterpret_cast<scsf_comm*>(cs[r]);
+  return SCSF_OK;
+}
+
+int scsf_comm_destroy(scsf_comm* c) {
+  delete reinterpret_cast<Comm*>(c);
+  return SCSF_OK;
+}
+
+int scsf_comm_rank(const scsf_comm* c, int32_t* rank, int32_t* world) {
+  SCSF_ARG_CHECK(c != nullptr, "comm is NULL");
+  const Comm* cc = reinterpret_cast<const Comm*>(c);
+  if (rank) *rank = cc->rank;
+  if (world) *world = cc->world;
+  return SCSF_OK;
+}
+
+void scsf_slab_rows(int32_t ny, int32_t world, int32_t rank, int32_t* y0, int32_t* y1) {
+  if (y0) *y0 = (int32_t)(((int64_t)rank * ny) / world);
+  if (y1) *y1 = (int32_t)(((int64_t)(rank + 1) * ny) / world);
+}
+
+static int check_dist(const scsf_ops* ops, int32_t y0, int32_t y1, const scsf_comm* comm) {
+  SCSF_ARG_CHECK(comm != nullptr, "comm is NULL");
+  SCSF_ARG_CHECK(ops->dim == 2, "the row-partitioned solve is 2-D (got dim %d)", ops->dim);
+  SCSF_ARG_CHECK(ops->nx % 4 == 0, "the row-partitioned solve needs nx %% 4 == 0 (got %d)", ops->nx);
+  SCSF_ARG_CHECK(0 <= y0 && y0 < y1 && y1 <= ops->ny, "slab rows [%d, %d) invalid for ny = %d", y0, y1, ops->ny);
+  const Comm* c = reinterpret_cast<const Comm*>(comm);
+  int32_t e0, e1;
+  scsf_slab_rows(ops->ny, c->world, c->rank, &e0, &e1);
+  SCSF_ARG_CHECK(e0 == y0 && e1 == y1, "slab rows [%d, %d) differ from scsf_slab_rows [%d, %d)", y0, y1, e0, e1);
+  return SCSF_OK;
+}
+
+size_t scsf_solve_dist_workspace_bytes(const scsf_ops* ops, int32_t y0, int32_t y1, int32_t L, int32_t nex,
+                                       int32_t world) {
+  if (!ops || world < 1 || y1 <= y0) return 0;
+  struct FakeComm final : Comm {
+    int allreduce_sum(double*, size_t, cudaStream_t) override { return 0; }
+    int allreduce_max_u64(unsigned long long*, size_t, cudaStream_t) override { return 0; }
+    int allgather(const double*, double*, size_t, cudaStream_t) override { return 0; }
+    int halo(const double*, const double*, double*, double*, size_t, cudaStream_t) override { return 0; }
+  } fake;
+  fake.world = world;
+  DistCtx d;
+  d.comm = &fake;
+  d.y0 = y0;
+  d.y1 = y1;
+  return solve_ws_bytes(ops, L, nex, &d);
+}
+
+int scsf_solve_queue_dist(const scsf_ops* ops, int32_t y0, int32_t y1, const int32_t* chain, int32_t n_chain,
+                          int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter, uint64_t seed,
+                          double* evals, double* evecs_local, int64_t ld_vec, scsf_stats* st, scsf_comm* comm,
+                          void* ws, size_t ws_bytes, void* stream) {
+  SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
+  SCSF_TRY(check_dist(ops, y0, y1, comm));
+  SCSF_TRY(check_queue(ops, chain, n_chain, evals, nullptr, ld_vec));
+  const int64_t n_loc = (int64_t)ops->nx * (y1 - y0);
+  SCSF_ARG_CHECK(evecs_local == nullptr || ld_vec >= n_loc, "ld_vec must be >= the slab's rows x nx");
+  if (n_chain == 0) return SCSF_OK;
+  SCSF_TRY(init_kernel_attrs());
+  DistCtx d;
+  d.comm = reinterpret_cast<Comm*>(comm);
+  d.y0 = y0;
+  d.y1 = y1;
+  SolveWS w;
+  SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w, &d));
+  return run_chain(ops, chain, n_chain, L, nex, degree, tol, max_iter, seed, evals, evecs_local, ld_vec, st, w,
+                   (cudaStream_t)stream);
 }
 
 }  // extern "C"

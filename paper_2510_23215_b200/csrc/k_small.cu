@@ -19,6 +19,26 @@
 
 namespace scsf {
 
+// Newton-refined fp64 reciprocal / reciprocal square root for normal, finite
+// arguments: MUFU seed + two Newton steps (no slow-path subroutine calls on
+// the round's critical path).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
 // ------------------------------------------------------------- chol_inv ----
 // Cholesky S = R^T R with the inverse factor built in the same elimination
 // sweep (Gauss-Jordan on [S | I]): at step j, row j of R = A[j, j:] / r_jj and
@@ -89,7 +109,7 @@ __global__ void __launch_bounds__(1024, 1) k_chol_reg(const double* __restrict__
       if (w == lj) {                                   // owner warp of row j
         const double d = __shfl_sync(0xffffffffu, sel<NS>(a, sj, sj), lj);
         const bool bad = !(d > 1e-14 * fabs(sdiag[j])) || !isfinite(d);
-        const double r = sqrt(d), rinv = 1.0 / r;
+        const double rinv = bad ? 0.0 : rsqrt_nr(d), r = d * rinv;
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
           const int k = l + 32 * q;
@@ -521,26 +541,6 @@ __device__ __forceinline__ int ins0(int a, int h) {    // insert a 0 bit at posi
   return ((a & ~lowmask) << 1) | (a & lowmask);
 }
 
-// Newton-refined fp64 reciprocal / reciprocal square root for normal, finite
-// arguments: MUFU seed + two Newton steps (no slow-path subroutine calls on
-// the round's critical path).
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y * fma(-h * y, y, 1.5);
-}
-
 template <int LOGB>
 __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__ Gin, int64_t ldg, int b,
                                                       double2* __restrict__ rec, int* __restrict__ recm,
@@ -762,7 +762,7 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
     const int j = base + lane;
     bool bad = false;
     if (j < b) {
-      const double r = res[j] / wn[j];
+      const double r = sqrt(res[j]) / sqrt(wn[j]);   // res, wn hold squared norms
       rel[j] = r;
       nonfin |= !isfinite(r);
       bad = !(r <= tol);
@@ -815,13 +815,14 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-__global__ void k_rand_block(double* __restrict__ V, int64_t ldv, int64_t n, int ncols, uint64_t seed) {
+__global__ void k_rand_block(double* __restrict__ V, int64_t ldv, int64_t n, int ncols, uint64_t seed,
+                             int64_t goff) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int j = blockIdx.y;
   if (k >= ldv || j >= ncols) return;
   double v = 0.0;
   if (k < n) {
-    uint64_t h = splitmix64(splitmix64(splitmix64(seed) ^ (uint64_t)j) ^ (uint64_t)k);
+    uint64_t h = splitmix64(splitmix64(splitmix64(seed) ^ (uint64_t)j) ^ (uint64_t)(k + goff));   // global row
     uint64_t h2 = splitmix64(h);
     double u1 = ((double)(h >> 11) + 1.0) * 0x1.0p-53;   // (0, 1]
     double u2 = (double)(h2 >> 11) * 0x1.0p-53;
@@ -894,6 +895,62 @@ __global__ void k_sub_upper(const double* __restrict__ A, int64_t lda, const dou
 __global__ void k_zero_block(double* __restrict__ P, int64_t ld, int rows, int cols) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
   if (i < rows && k < cols) P[i + k * ld] = 0.0;
+}
+
+// Row-partitioned sign convention: per column, the local largest |.| entry
+// (first global index on ties) -> colbuf[3 j] = (|v|, global index, v); after
+// the all-gather every rank picks the same winner and applies its sign.
+__global__ void __launch_bounds__(256) k_colmax_local(const double* __restrict__ V, int64_t ldv, int64_t n,
+                                                      const int* __restrict__ perm, int64_t goff,
+                                                      double* __restrict__ colbuf) {
+  const int j = blockIdx.x;
+  const double* v = V + (int64_t)perm[j] * ldv;
+  double best = -1.0;
+  int64_t bi = 0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double a = fabs(v[k]);
+    if (a > best) { best = a; bi = k; }
+  }
+  __shared__ double sb[256];
+  __shared__ int64_t si[256];
+  sb[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double b2 = sb[threadIdx.x + o];
+      const int64_t i2 = si[threadIdx.x + o];
+      if (b2 > sb[threadIdx.x] || (b2 == sb[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sb[threadIdx.x] = b2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    colbuf[3 * j] = sb[0];
+    colbuf[3 * j + 1] = (double)(si[0] + goff);
+    colbuf[3 * j + 2] = (n > 0) ? v[si[0]] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sign_apply(const double* __restrict__ V, int64_t ldv, int64_t n,
+                                                    const int* __restrict__ perm, const double* __restrict__ gath,
+                                                    int world, int b, double* __restrict__ Out, int64_t ldo) {
+  const int j = blockIdx.x;
+  double best = -1.0, bidx = 0.0, bval = 1.0;
+  for (int r = 0; r < world; ++r) {                   // ranks own increasing global rows
+    const double* c = gath + (size_t)r * 3 * b + 3 * j;
+    if (c[0] > best || (c[0] == best && c[1] < bidx)) {
+      best = c[0];
+      bidx = c[1];
+      bval = c[2];
+    }
+  }
+  const double sgn = (bval < 0.0) ? -1.0 : 1.0;
+  const double* v = V + (int64_t)perm[j] * ldv;
+  double* o = Out + (int64_t)j * ldo;
+  for (int64_t k = threadIdx.x; k < ldo && k < ldv; k += blockDim.x) o[k] = (k < n) ? sgn * v[k] : 0.0;
 }
 
 // ------------------------------------------------------------------ host ----
@@ -1042,9 +1099,28 @@ int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s) 
   return SCSF_OK;
 }
 
-int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, cudaStream_t s) {
+int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s) {
   dim3 g(ceil_div(ldv, 256), ncols);
-  k_rand_block<<<g, 256, 0, s>>>(V, ldv, n, ncols, seed);
+  k_rand_block<<<g, 256, 0, s>>>(V, ldv, n, ncols, seed, goff);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+int colmax_local_impl(const double* V, int64_t ldv, int64_t n, const int* perm, int b, int64_t goff, double* colbuf,
+                      cudaStream_t s) {
+  k_colmax_local<<<b, 256, 0, s>>>(V, ldv, n, perm, goff, colbuf);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+int sort_theta_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
+                    Ctrl* ctrl, cudaStream_t s) {
+  k_sort_theta<<<1, 512, 0, s>>>(theta, rel, b, L, perm, theta_sorted, ctrl);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+int sign_apply_impl(const double* V, int64_t ldv, int64_t n, const int* perm, const double* gath, int world, int b,
+                    double* Out, int64_t ldo, cudaStream_t s) {
+  k_sign_apply<<<b, 256, 0, s>>>(V, ldv, n, perm, gath, world, b, Out, ldo);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

@@ -614,8 +614,98 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   }
 }
 
+// ------------------------------------------------ row-partitioned (slab) ----
+// Row partition of a 2-D operator: this rank owns grid rows
+// [y0, y1); vectors hold only those n_loc = nx (y1 - y0) rows, the operator
+// arrays stay global (coefficient index = goff + local index, goff = y0 nx).
+// The rows just outside the slab come from the neighbours' boundary rows
+// (halo, comm.cu): ghost_lo [ncols][nx] = row y0 - 1, ghost_hi = row y1.
+// pack: send_lo [ncols][nx] = first own row, send_hi = last own row.
+__global__ void k_pack_rows(const double* __restrict__ X, int64_t ldv, int64_t n_loc, int nx, int ncols,
+                            double* __restrict__ send_lo, double* __restrict__ send_hi) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (x >= nx || j >= ncols) return;
+  const double* col = X + (int64_t)j * ldv;
+  send_lo[(int64_t)j * nx + x] = col[x];
+  send_hi[(int64_t)j * nx + x] = col[n_loc - nx + x];
+}
+
+// One filter step (or A X when step < 0) on a slab, 4 points per thread (nx % 4 == 0).
+template <int CB>
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
+    const double* __restrict__ cf, int64_t ldc, int nx, int64_t n_glob, int64_t goff, int64_t n_loc,
+    const double* __restrict__ X, const double* Xp, double* Out, int64_t ldv, int ncols,
+    const double* __restrict__ ghost_lo, const double* __restrict__ ghost_hi, const double* __restrict__ fp,
+    int step) {
+  const int64_t l0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;   // local point
+  if (l0 >= ldv) return;
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int j0 = blockIdx.y * CB;
+  const int j1 = min(ncols, j0 + CB);
+  if (l0 >= n_loc) {                                  // ld padding
+    for (int j = j0; j < j1; ++j) stg4(Out + (int64_t)j * ldv + l0, make_double4(0, 0, 0, 0));
+    return;
+  }
+  const int64_t k0 = goff + l0;                       // global point
+  const double4 dg = ldg4_nc(cf + k0);
+  const double4 cxp = ldg4_nc(cf + ldc + k0);
+  const double cxm = (k0 >= 1) ? cf[ldc + k0 - 1] : 0.0;
+  const double4 cyp = ldg4_nc(cf + 2 * ldc + k0);
+  const bool hym = k0 >= nx, hyp = k0 + nx < n_glob;  // global Dirichlet boundary
+  const double4 cym = hym ? ldg4_nc(cf + 2 * ldc + k0 - nx) : make_double4(0, 0, 0, 0);
+  const bool hm = l0 >= 1, hp = l0 + 4 < n_loc;       // x-neighbours never leave the slab row
+  const bool dn_in = l0 >= nx, up_in = l0 + nx < n_loc;
+#pragma unroll
+  for (int jj = 0; jj < CB; ++jj) {
+    const int j = j0 + jj;
+    if (j >= j1) break;
+    const double* __restrict__ x = X + (int64_t)j * ldv;
+    const double4 xc = ldg4_nc(x + l0);
+    const double xl = hm ? x[l0 - 1] : 0.0;
+    const double xr = hp ? x[l0 + 4] : 0.0;
+    double4 xu = make_double4(0, 0, 0, 0), xd = make_double4(0, 0, 0, 0);
+    if (hyp) xu = up_in ? ldg4_nc(x + l0 + nx) : ldg4_nc(ghost_hi + (int64_t)j * nx + (l0 + nx - n_loc));
+    if (hym) xd = dn_in ? ldg4_nc(x + l0 - nx) : ldg4_nc(ghost_lo + (int64_t)j * nx + l0);
+    double4 v;
+    v.x = (dg.x - c) * xc.x + cxp.x * xc.y + cxm * xl + cyp.x * xu.x + cym.x * xd.x;
+    v.y = (dg.y - c) * xc.y + cxp.y * xc.z + cxp.x * xc.x + cyp.y * xu.y + cym.y * xd.y;
+    v.z = (dg.z - c) * xc.z + cxp.z * xc.w + cxp.y * xc.y + cyp.z * xu.z + cym.z * xd.z;
+    v.w = (dg.w - c) * xc.w + cxp.w * xr + cxp.z * xc.z + cyp.w * xu.w + cym.w * xd.w;
+    v.x *= a; v.y *= a; v.z *= a; v.w *= a;
+    if (b != 0.0) {
+      const double4 p = ldg4(Xp + (int64_t)j * ldv + l0);
+      v.x = fma(b, p.x, v.x); v.y = fma(b, p.y, v.y); v.z = fma(b, p.z, v.z); v.w = fma(b, p.w, v.w);
+    }
+    stg4(Out + (int64_t)j * ldv + l0, v);
+  }
+}
+
+int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncols, double* send_lo,
+                   double* send_hi, cudaStream_t s) {
+  if (ncols <= 0) return SCSF_OK;
+  k_pack_rows<<<dim3(ceil_div(nx, 128), ncols), 128, 0, s>>>(X, ldv, n_loc, nx, ncols, send_lo, send_hi);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
+                      double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
+                      const double* fp, int step, cudaStream_t s) {
+  if (ncols <= 0) return SCSF_OK;
+  const int64_t n_glob = (int64_t)ops->nx * ops->ny;
+  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  constexpr int CB = 2;
+  dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
+  k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
+                                              ghost_lo, ghost_hi, fp, step);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
 // ---------------------------------------------------------- residuals ----
-// For active column j: res[j] = ||W_j - theta_j V_j||_2, wn[j] = ||W_j||_2 (fixed-order sums).
+// For active column j: res[j] = ||W_j - theta_j V_j||_2^2, wn[j] = ||W_j||_2^2 (fixed-order sums;
+// squared so a row-partitioned solve can all-reduce them; k_lock takes the roots).
 __global__ void __launch_bounds__(512) k_resid(const double* __restrict__ V, const double* __restrict__ W,
                                                int64_t ldv, int64_t n, const double* __restrict__ theta,
                                                double* __restrict__ res, double* __restrict__ wn) {
@@ -654,8 +744,8 @@ __global__ void __launch_bounds__(512) k_resid(const double* __restrict__ V, con
       a += sr[i];
       bb += sw[i];
     }
-    res[j] = sqrt(a);
-    wn[j] = sqrt(bb);
+    res[j] = a;                                       // squared: summed over ranks (row partition) before sqrt
+    wn[j] = bb;
   }
 }
 

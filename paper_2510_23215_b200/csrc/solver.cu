@@ -13,6 +13,7 @@
 // The host reads the device control block once per iteration (kL drives the
 // launch shapes of the next iteration).
 #include "solver.cuh"
+#include "comm.cuh"
 
 #include <algorithm>
 #include <utility>
@@ -43,12 +44,34 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
               double tol, Ctrl* ctrl, double* fp, cudaStream_t s);
 int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
-int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, cudaStream_t s);
+int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s);
+int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncols, double* send_lo,
+                   double* send_hi, cudaStream_t s);
+int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
+                      double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
+                      const double* fp, int step, cudaStream_t s);
+int colmax_local_impl(const double* V, int64_t ldv, int64_t n, const int* perm, int b, int64_t goff, double* colbuf,
+                      cudaStream_t s);
+int sort_theta_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
+                    Ctrl* ctrl, cudaStream_t s);
+int sign_apply_impl(const double* V, int64_t ldv, int64_t n, const int* perm, const double* gath, int world, int b,
+                    double* Out, int64_t ldo, cudaStream_t s);
 int finalize_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
                   const double* V, int64_t ldv, int64_t n, double* Out, int64_t ldo, Ctrl* ctrl,
                   cudaStream_t s);
 
-static void carve(Arena& a, SolveWS& w, int64_t n, int b) {
+static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCtx* dist) {
+  const int64_t n_glob = (int64_t)ops->nx * ops->ny * ops->nz;
+  int64_t n = n_glob;
+  w.n_glob = n_glob;
+  w.goff = 0;
+  w.comm = nullptr;
+  w.nx = ops->nx;
+  if (dist && dist->comm) {
+    n = (int64_t)ops->nx * (dist->y1 - dist->y0);
+    w.goff = (int64_t)ops->nx * dist->y0;
+    w.comm = dist->comm;
+  }
   w.n = n;
   w.b = b;
   w.ldv = round_up(n, 32);
@@ -73,18 +96,28 @@ static void carve(Arena& a, SolveWS& w, int64_t n, int b) {
   w.perm = a.take<int>(b);
   w.ctrl = a.take<Ctrl>(1);
   w.gersh = a.take<unsigned long long>(1);
+  if (dist && dist->comm) {
+    const int64_t hb = (int64_t)b * ops->nx;
+    w.send_lo = a.take<double>(hb);
+    w.send_hi = a.take<double>(hb);
+    w.recv_lo = a.take<double>(hb);
+    w.recv_hi = a.take<double>(hb);
+    w.colbuf = a.take<double>(3 * (int64_t)b);
+    w.colgath = a.take<double>(3 * (int64_t)b * dist->comm->world);
+  }
 }
 
-size_t solve_ws_bytes(const scsf_ops* ops, int L, int nex) {
+size_t solve_ws_bytes(const scsf_ops* ops, int L, int nex, const DistCtx* dist) {
   Arena a(nullptr, 0);
   SolveWS w;
-  carve(a, w, (int64_t)ops->nx * ops->ny * ops->nz, L + nex);
+  carve(a, w, ops, L + nex, dist);
   return a.off;
 }
 
-int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_bytes, SolveWS& w) {
+int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_bytes, SolveWS& w,
+                   const DistCtx* dist) {
   Arena a(ws, ws_bytes);
-  carve(a, w, (int64_t)ops->nx * ops->ny * ops->nz, L + nex);
+  carve(a, w, ops, L + nex, dist);
   if (a.overflow || ws == nullptr) {
     set_error("workspace too small: need %zu bytes, got %zu", a.off, ws_bytes);
     return SCSF_ERR_WORKSPACE;
@@ -92,10 +125,29 @@ int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_byte
   return SCSF_OK;
 }
 
+// ---- the exchange points of the row-partitioned solve (no-ops on one GPU) ----
+// C = X^T Y summed over ranks (Gram / projection blocks, Alg. 3 ll. 4-5)
+static int gram(SolveWS& w, const double* X, int b1, const double* Y, int b2, int sym, double* C,
+                cudaStream_t s) {
+  SCSF_TRY(gemm_tn(X, w.ldv, b1, Y, w.ldv, b2, w.n, 1.0, sym, C, b1, w.P, s));
+  if (w.comm) SCSF_TRY(w.comm->allreduce_sum(C, (size_t)b1 * b2, s));
+  return SCSF_OK;
+}
+
+// One stencil application (filter step `step`, or A X when step < 0) on ncols columns.
+static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const double* Xp, double* Out, int ncols,
+                int step, cudaStream_t s) {
+  if (!w.comm) return stencil_impl(ops, op, X, Xp, Out, w.ldv, ncols, w.fp, step, s);
+  SCSF_TRY(pack_rows_impl(X, w.ldv, w.n, w.nx, ncols, w.send_lo, w.send_hi, s));
+  SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
+  return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, w.comm->rank > 0 ? w.recv_lo : nullptr,
+                           w.comm->rank + 1 < w.comm->world ? w.recv_hi : nullptr, w.fp, step, s);
+}
+
 // Q = CholQR pass on columns [0, ncols) of Y (in place, or into Out when Out != Y).
 static int cholqr_pass(SolveWS& w, double* Y, double* Out, int ncols, cudaStream_t s) {
-  SCSF_TRY(gemm_tn(Y, w.ldv, ncols, Y, w.ldv, ncols, w.n, 1.0, 1, w.S, ncols, w.P, s));
-  SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n, w.Rinv, w.Gwork, w.ctrl, s));
+  SCSF_TRY(gram(w, Y, ncols, Y, ncols, 1, w.S, s));
+  SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n_glob, w.Rinv, w.Gwork, w.ctrl, s));
   SCSF_TRY(gemm_nn_ex(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, 1, s));
   return SCSF_OK;
 }
@@ -107,13 +159,17 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
   const int ba = w.b - k0;
   double* Va = w.V + (int64_t)k0 * w.ldv;
   double* Wa = w.W + (int64_t)k0 * w.ldv;
-  SCSF_TRY(stencil_impl(ops, op, Va, nullptr, Wa, w.ldv, ba, w.fp, -1, s));
+  SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
   spmm_cols += ba;
-  SCSF_TRY(gemm_tn(Va, w.ldv, ba, Wa, w.ldv, ba, w.n, 1.0, 1, w.S, ba, w.P, s));
+  SCSF_TRY(gram(w, Va, ba, Wa, ba, 1, w.S, s));
   SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Va, w.ldv, s));
   SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
   SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
+  if (w.comm) {
+    SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
+    SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
+  }
   SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
   return SCSF_OK;
 }
@@ -194,7 +250,7 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
   Ctrl h{};
   SCSF_TRY(gershgorin_impl(ops, op, w.gersh, s));
   SCSF_TRY(ctrl_init_impl(w.ctrl, w.gersh, s));
-  if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, s));
+  if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, w.goff, s));
   if (!warm || orthonormalize) {
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
@@ -211,14 +267,13 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
     // 1. Chebyshev filter (Alg. 1) on the active block
     SCSF_TRY(tm.mark(0, s));
     double* F;
-    if (filter_resident_ok(ops)) {
+    if (!w.comm && filter_resident_ok(ops)) {
       SCSF_TRY(filter_resident_impl(ops, op, y[0], y[1], w.ldv, ba, w.fp, degree, s));
       F = y[1];
     } else {
-      SCSF_TRY(stencil_impl(ops, op, y[0], nullptr, y[1], w.ldv, ba, w.fp, 0, s));
+      SCSF_TRY(spmm(ops, op, w, y[0], nullptr, y[1], ba, 0, s));
       for (int st_i = 1; st_i < degree; ++st_i)
-        SCSF_TRY(stencil_impl(ops, op, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], w.ldv, ba, w.fp,
-                              st_i, s));
+        SCSF_TRY(spmm(ops, op, w, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], ba, st_i, s));
       F = y[degree % 3];
     }
     SCSF_TRY(tm.mark(1, s));
@@ -230,7 +285,7 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
     // 2. block classical Gram-Schmidt, twice, against the locked vectors
     if (kL > 0) {
       for (int rep = 0; rep < 2; ++rep) {
-        SCSF_TRY(gemm_tn(w.V, w.ldv, kL, F, w.ldv, ba, w.n, 1.0, 0, w.C, kL, w.P, s));
+        SCSF_TRY(gram(w, w.V, kL, F, ba, 0, w.C, s));
         SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kL, w.C, kL, ba, -1.0, 1.0, F, w.ldv, s));
       }
     }
@@ -256,8 +311,15 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
     kL = h.kL;
   }
   // final ascending order + sign convention into T1, then swap so V holds it
-  SCSF_TRY(finalize_impl(w.theta, w.rel, b, L, w.perm, w.theta_sorted, w.V, w.ldv, w.n, w.T1, w.ldv,
-                         w.ctrl, s));
+  if (w.comm) {
+    SCSF_TRY(sort_theta_impl(w.theta, w.rel, b, L, w.perm, w.theta_sorted, w.ctrl, s));
+    SCSF_TRY(colmax_local_impl(w.V, w.ldv, w.n, w.perm, b, w.goff, w.colbuf, s));
+    SCSF_TRY(w.comm->allgather(w.colbuf, w.colgath, 3 * (size_t)b, s));
+    SCSF_TRY(sign_apply_impl(w.V, w.ldv, w.n, w.perm, w.colgath, w.comm->world, b, w.T1, w.ldv, s));
+  } else {
+    SCSF_TRY(finalize_impl(w.theta, w.rel, b, L, w.perm, w.theta_sorted, w.V, w.ldv, w.n, w.T1, w.ldv,
+                           w.ctrl, s));
+  }
   std::swap(w.V, w.T1);
   SCSF_TRY(read_ctrl(w, h, s));
   int status = SCSF_OK;

@@ -135,3 +135,39 @@ def gather_evals(evals: torch.Tensor, chain: np.ndarray, N: int, L: int):
     for e, i, cnt in zip(ge, gi, counts):
         out[i[:cnt].cpu()] = e[:cnt].cpu()
     return out
+
+
+# ------------------------------------------------- row-partitioned operator ----
+# configs[4] / SURVEY §8(a) a11: one operator's grid rows split over the ranks
+# (scsf_solve_queue_dist); the NCCL communicator is bootstrapped here.
+def make_comm(rank: int, world: int, uid_fn=None, create_fn=None):
+    """NCCL communicator of this rank: rank 0 makes the 128-byte unique id, torch.distributed
+    broadcasts it (any backend), every rank builds its communicator from it."""
+    import torch.distributed as dist
+    uid_fn = uid_fn or scsf.comm_unique_id
+    create_fn = create_fn or scsf.comm_create
+    box = [uid_fn() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(box, src=0)
+    return create_fn(rank, world, box[0])
+
+
+def slab_partition(ny: int, world: int) -> list[tuple[int, int]]:
+    """Rows [y0, y1) of every rank (scsf_slab_rows; contiguous, sizes differ by at most 1)."""
+    return [((r * ny) // world, ((r + 1) * ny) // world) for r in range(world)]
+
+
+def gather_slabs(evecs_local: torch.Tensor, nx: int, rows: tuple[int, int], ny: int):
+    """All-gather every rank's slab rows of [n_chain, L, ld_loc] eigenvectors into [n_chain, L, nx ny]."""
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    y0, y1 = rows
+    n_loc = nx * (y1 - y0)
+    parts = slab_partition(ny, world)
+    maxrows = max(b - a for a, b in parts)
+    nc, L = evecs_local.shape[0], evecs_local.shape[1]
+    pad = torch.zeros((nc, L, nx * maxrows), dtype=evecs_local.dtype, device=evecs_local.device)
+    pad[:, :, :n_loc] = evecs_local[:, :, :n_loc]
+    got = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(got, pad)
+    return torch.cat([g[:, :, :nx * (b - a)] for g, (a, b) in zip(got, parts)], dim=2)

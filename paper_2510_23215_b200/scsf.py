@@ -27,6 +27,8 @@ EXPORTED = [
     "scsf_solve_one", "scsf_solve_queue", "scsf_last_error", "scsf_abi_version",
     "scsf_launch_count", "scsf_set_timing", "scsf_solve_chains",
     "scsf_dev_workspace_bytes", "scsf_gemm_tn", "scsf_gemm_nn", "scsf_chol_inv", "scsf_syev_small",
+    "scsf_comm_unique_id", "scsf_comm_create", "scsf_comm_create_loopback", "scsf_comm_destroy",
+    "scsf_comm_rank", "scsf_slab_rows", "scsf_solve_dist_workspace_bytes", "scsf_solve_queue_dist",
 ]
 
 
@@ -96,6 +98,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_gemm_nn": (ctypes.c_int, [P, I64, I64, I32, P, I64, I32, D, D, P, I64, P]),
         "scsf_chol_inv": (ctypes.c_int, [P, I64, I32, I64, P, P, SZ, P]),
         "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, P, SZ, P]),
+        "scsf_comm_unique_id": (ctypes.c_int, [P]),
+        "scsf_comm_create": (ctypes.c_int, [I32, I32, P, ctypes.POINTER(P)]),
+        "scsf_comm_create_loopback": (ctypes.c_int, [I32, P]),
+        "scsf_comm_destroy": (ctypes.c_int, [P]),
+        "scsf_comm_rank": (ctypes.c_int, [P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "scsf_slab_rows": (None, [I32, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "scsf_solve_dist_workspace_bytes": (SZ, [OPS, I32, I32, I32, I32, I32]),
+        "scsf_solve_queue_dist": (ctypes.c_int, [OPS, I32, I32, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P,
+                                                 P, I64, ST, P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -367,3 +378,76 @@ def syev_small(G: torch.Tensor, return_sweeps: bool = False):
     _check(lib.scsf_syev_small(_ptr(G), b, b, _ptr(theta), _ptr(Z), ctypes.byref(sw), _ptr(ws), ws.numel(),
                                _stream()))
     return (theta, Z, sw.value) if return_sweeps else (theta, Z)
+
+
+# ------------------------------------------------- row-partitioned solve ----
+def slab_rows(ny: int, world: int, rank: int) -> tuple[int, int]:
+    """Grid rows [y0, y1) owned by `rank` (scsf_slab_rows)."""
+    lib = load_library()
+    y0, y1 = ctypes.c_int32(0), ctypes.c_int32(0)
+    lib.scsf_slab_rows(ny, world, rank, ctypes.byref(y0), ctypes.byref(y1))
+    return y0.value, y1.value
+
+
+class Comm:
+    """Owning handle of a scsf_comm (NCCL or loopback)."""
+
+    def __init__(self, handle):
+        self.handle = ctypes.c_void_p(handle)
+        r, w = ctypes.c_int32(0), ctypes.c_int32(0)
+        _check(load_library().scsf_comm_rank(self.handle, ctypes.byref(r), ctypes.byref(w)))
+        self.rank, self.world = r.value, w.value
+
+    def close(self):
+        if self.handle:
+            load_library().scsf_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p(None)
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 makes it; broadcast it with torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().scsf_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_create(rank: int, world: int, uid: bytes) -> Comm:
+    """NCCL communicator over NVLink/NVSwitch (collective: every rank calls it)."""
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    h = ctypes.c_void_p(None)
+    _check(load_library().scsf_comm_create(rank, world, buf, ctypes.byref(h)))
+    return Comm(h.value)
+
+
+def comm_create_loopback(world: int) -> list[Comm]:
+    """`world` in-process virtual ranks on the current device (tests / one-GPU parity)."""
+    arr = (ctypes.c_void_p * world)()
+    _check(load_library().scsf_comm_create_loopback(world, arr))
+    return [Comm(arr[r]) for r in range(world)]
+
+
+def solve_queue_dist(ops: Operators, chain, L: int, nex: int, comm: Comm, degree: int = 20, tol: float = 1e-8,
+                     max_iter: int = 200, seed: int = 0, want_vecs: bool = True, raise_on_fail=True,
+                     stream: torch.cuda.Stream | None = None):
+    """Row-partitioned SCSF chain solve on this rank's slab (scsf_solve_queue_dist).
+
+    Returns (evals[n_chain, L], evecs_local[n_chain, L, ld_loc] or None, stats list, (y0, y1))."""
+    lib = load_library()
+    chain = np.ascontiguousarray(np.asarray(chain, dtype=np.int32))
+    nc = int(chain.shape[0])
+    y0, y1 = slab_rows(ops.ny, comm.world, comm.rank)
+    st = ops.c_struct()
+    dev = ops.coef.device
+    ws = _workspace(lib.scsf_solve_dist_workspace_bytes(ctypes.byref(st), y0, y1, L, nex, comm.world), dev)
+    n_loc = ops.nx * (y1 - y0)
+    ld_loc = ld_for(n_loc)
+    evals = torch.empty((nc, L), dtype=torch.float64, device=dev)
+    evecs = torch.empty((nc, L, ld_loc), dtype=torch.float64, device=dev) if want_vecs else None
+    stats = (scsf_stats * max(nc, 1))()
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    code = lib.scsf_solve_queue_dist(ctypes.byref(st), y0, y1, chain.ctypes.data_as(ctypes.c_void_p), nc, L, nex,
+                                     degree, tol, max_iter, ctypes.c_uint64(seed), _ptr(evals), _ptr(evecs), ld_loc,
+                                     stats, comm.handle, _ptr(ws), ws.numel(), s)
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return evals, evecs, [stats[i].as_dict() for i in range(nc)], (y0, y1)

@@ -1,5 +1,6 @@
 """Per-phase time per operator with C concurrent chains (phase timers on): shows which phase
 stretches under contention.   python tools/chain_phases.py [CFG] [N_OPS] [CHAINS...]"""
+import resource
 import sys
 import time
 
@@ -26,20 +27,26 @@ def main():
         for timing in (False, True):
             scsf.set_timing(timing)
             torch.cuda.synchronize()
+            ru0 = resource.getrusage(resource.RUSAGE_SELF)
             t0 = time.perf_counter()
             _, _, st = scsf.solve_chains(ops, perm, C, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=1,
                                          want_vecs=False, raise_on_fail=False)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            ru1 = resource.getrusage(resource.RUSAGE_SELF)
+            cpu = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
             if not timing:
                 rate = nops / dt
+                cpu_frac = cpu / dt
+                launches = scsf.launch_count()
                 continue
             f_ms = np.mean([s["t_filter_ms"] for s in st])
             o_ms = np.mean([s["t_ortho_ms"] for s in st])
             r_ms = np.mean([s["t_rr_ms"] for s in st])
             per_op_chain = dt * 1e3 * C / nops
             print(f"{name} chains={C:3d}: {rate:7.1f} ops/s (untimed); per op per chain {per_op_chain:6.2f} ms: "
-                  f"filter {f_ms:5.2f}  ortho {o_ms:5.2f}  rr {r_ms:5.2f}  other {per_op_chain - f_ms - o_ms - r_ms:5.2f}")
+                  f"filter {f_ms:5.2f}  ortho {o_ms:5.2f}  rr {r_ms:5.2f}  other {per_op_chain - f_ms - o_ms - r_ms:5.2f}"
+                  f"  | host cores busy {cpu_frac:4.1f}")
     scsf.set_timing(False)
 
 
