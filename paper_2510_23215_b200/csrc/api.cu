@@ -22,8 +22,13 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
-void count_launch(int n) { g_launches += n; }
+static thread_local bool t_capturing = false;
+void set_capturing(bool on) { t_capturing = on; }
+void count_launch(int n) {
+  if (!t_capturing) g_launches += n;
+}
 bool debug_sync() {
+  if (t_capturing) return false;
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SCSF_DEBUG_SYNC");
@@ -54,9 +59,11 @@ int set_timing(int on);
 // k_small.cu / k_dense.cu: one-time kernel attributes (set before any worker thread starts)
 int set_small_attrs();
 int dense_init_attrs();
+int stencil_init_attrs();
 static int init_kernel_attrs() {
   SCSF_TRY(set_small_attrs());
   SCSF_TRY(dense_init_attrs());
+  SCSF_TRY(stencil_init_attrs());
   return SCSF_OK;
 }
 // k_stencil.cu
@@ -299,8 +306,16 @@ int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   SCSF_TRY(init_kernel_attrs());
   SolveWS w;
   SCSF_TRY(carve_solve_ws(ops, L, nex, ws, ws_bytes, w));
-  return run_chain(ops, chain, n_chain, L, nex, degree, tol, max_iter, seed, evals, evecs, ld_vec, st, w,
-                   (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (s != nullptr) return run_chain(ops, chain, n_chain, L, nex, degree, tol, max_iter, seed, evals, evecs, ld_vec, st, w, s);
+  // the legacy default stream cannot be captured into a graph: run on a private stream
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(nullptr));
+  cudaStream_t ps = nullptr;
+  SCSF_CUDA_CHECK(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+  const int r = run_chain(ops, chain, n_chain, L, nex, degree, tol, max_iter, seed, evals, evecs, ld_vec, st, w, ps);
+  cudaStreamSynchronize(ps);
+  cudaStreamDestroy(ps);
+  return r;
 }
 
 int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start, int32_t n_chains,

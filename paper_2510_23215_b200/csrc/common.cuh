@@ -12,6 +12,7 @@ namespace scsf {
 // ---------------------------------------------------------------- errors ----
 void set_error(const char* fmt, ...);
 void count_launch(int n = 1);
+void set_capturing(bool on);   // launches inside a CUDA-graph capture are counted at replay
 bool debug_sync();   // SCSF_DEBUG_SYNC=1: synchronise and check after every launch
 
 struct Status {

@@ -88,13 +88,13 @@ __global__ void __launch_bounds__(128) k_gemm_tn(const double* __restrict__ X, i
 // the 8 warp sums are then added in warp order: a fixed order, so deterministic.
 // Symmetric results (Gram, Rayleigh quotient) are read as upper triangles by their consumers.
 __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ P, int splits, int b1,
-                                                         int b2, double alpha, int upper, double* __restrict__ C,
-                                                         int64_t ldc) {
+                                                         int b2, double alpha, int upper_cols,
+                                                         double* __restrict__ C, int64_t ldc) {
   __shared__ double part[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   const int j = blockIdx.y;
-  if (upper && blockIdx.x * 32 > j) return;          // tile strictly below the diagonal
+  if (j < upper_cols && (int)blockIdx.x * 32 > j) return;   // tile strictly below the diagonal
   const int64_t stride = (int64_t)b1 * b2;
   double s = 0.0;
   if (i < b1) {
@@ -194,13 +194,20 @@ constexpr int V2_T = 64, V2_KC = 32, V2_P = V2_KC + 4;   // tile, k-chunk, pitch
 // ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
 __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
                                                   const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
-                                                  int64_t kchunk, int upper, int a16, double* __restrict__ P) {
+                                                  int64_t kchunk, int upper, int a16, double* __restrict__ P,
+                                                  const double* __restrict__ Y2) {
   extern __shared__ __align__(16) double smd[];
   double* xs = smd;                                  // [2][64][36]
   double* ys = smd + 2 * V2_T * V2_P;                // [2][64][36]
-  const int ti = blockIdx.x, tj = blockIdx.y;
-  if (upper && ti > tj) return;
+  // dual mode (Y2 != NULL): output columns [0, b2) = X^T Y (upper rule), [b2, 2 b2) = X^T Y2 (full)
+  const int T2 = (b2 + V2_T - 1) / V2_T;
+  const int grp = Y2 ? (int)blockIdx.y / T2 : 0;
+  const int ti = blockIdx.x, tj = Y2 ? (int)blockIdx.y % T2 : (int)blockIdx.y;
+  if (upper && grp == 0 && ti > tj) return;
+  if (grp) Y = Y2;
   const int i0 = ti * V2_T, j0 = tj * V2_T;
+  const int b2tot = Y2 ? 2 * b2 : b2;
+  const int jout = grp * b2;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min(n, kbeg + kchunk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
     }
     __syncthreads();
   }
-  double* out = P + (int64_t)blockIdx.z * b1 * b2;
+  double* out = P + (int64_t)blockIdx.z * b1 * b2tot;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + 2 * t + e;
-        if (i < b1 && j < b2) out[i + (int64_t)j * b1] = acc[mi][ni][e];
+        if (i < b1 && j < b2) out[i + (int64_t)(j + jout) * b1] = acc[mi][ni][e];
       }
 }
 
@@ -427,7 +434,7 @@ int tn_splits(int64_t n, int b1, int b2) {
 // splits * b1' * b2' <= 2 * 296 * 64^2 + b1' * b2'.
 size_t tn_partial_doubles(int64_t n, int b1, int b2) {
   (void)n;
-  return (size_t)4 * 148 * TN_BM * TN_BM + (size_t)b1 * b2;
+  return (size_t)4 * 148 * TN_BM * TN_BM + (size_t)2 * b1 * b2;     // 2 b1 b2: the dual (two-Y) mode
 }
 
 // C (b1 x b2, ldc) = alpha X^T Y.  P: workspace of tn_partial_doubles.
@@ -447,10 +454,32 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
   const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
-  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P);
+  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b1, 32), b2);
-  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper, C, ldc);
+  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper ? b2 : 0, C, ldc);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+// One pass over X for two products: C[:, 0:b) = X^T Y1 (upper triangle; X == Y1),
+// C[:, b:2b) = X^T Y2 (full).  C is b x 2b (ldc >= b).
+int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y2, int64_t ldy, int b, int64_t n,
+                 double* C, int64_t ldc, double* P, cudaStream_t s) {
+  if (b <= 0) return SCSF_OK;
+  SCSF_TRY(dense_init_attrs());
+  const int t = ceil_div(b, V2_T);
+  const int tiles = t * (t + 1) / 2 + t * t;
+  int splits = min(max(1, ceil_div(n, 128)), max(1, (2 * 148 + tiles - 1) / tiles));
+  int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
+  splits = ceil_div(n, kchunk);
+  dim3 g(t, 2 * t, splits);
+  const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
+                   ((uintptr_t)Y2 & 15) == 0) ? 1 : 0;
+  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b, Y1, ldy, b, n, kchunk, 1, a16, P, Y2);
+  SCSF_LAUNCH_CHECK();
+  dim3 gr(ceil_div(b, 32), 2 * b);
+  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b, 2 * b, 1.0, b, C, ldc);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

@@ -787,12 +787,6 @@ bool filter_resident_ok(const scsf_ops* ops) {
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_filter_cl<CS, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
 }
 template <int CS>
@@ -810,6 +804,27 @@ static cudaError_t launch_cl(cudaLaunchConfig_t& cfg, int cs, int cb, const doub
     case 4: return launch_cl_cb<4>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
     default: return launch_cl_cb<8>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
   }
+}
+
+// All dynamic-shared-memory opt-ins of the filter kernels, set once before any
+// launch (in particular before a CUDA-graph capture).
+int stencil_init_attrs() {
+  static bool done = false;
+  if (done) return SCSF_OK;
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * RES_MAX_N * (int)sizeof(double)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * 4 * RQ_T * RQ_Q * (int)sizeof(double)));
+#define SCSF_CL_ATTR(CS, CB) \
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+  SCSF_CL_ATTR(1, 1); SCSF_CL_ATTR(1, 2); SCSF_CL_ATTR(1, 4);
+  SCSF_CL_ATTR(2, 1); SCSF_CL_ATTR(2, 2); SCSF_CL_ATTR(2, 4);
+  SCSF_CL_ATTR(4, 1); SCSF_CL_ATTR(4, 2); SCSF_CL_ATTR(4, 4);
+  SCSF_CL_ATTR(8, 1); SCSF_CL_ATTR(8, 2); SCSF_CL_ATTR(8, 4);
+#undef SCSF_CL_ATTR
+  g_res_attr = 1;
+  done = true;
+  return SCSF_OK;
 }
 
 // Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.

@@ -16,7 +16,12 @@
 #include "comm.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <utility>
+#include <vector>
 
 namespace scsf {
 
@@ -36,6 +41,8 @@ int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, in
 int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
                double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s);
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
+int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y2, int64_t ldy, int b, int64_t n,
+                 double* C, int64_t ldc, double* P, cudaStream_t s);
 size_t small_scratch_doubles(int b);
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
                   Ctrl* ctrl, cudaStream_t s);
@@ -86,6 +93,9 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.Zwork = a.take<double>(bb);
   w.Gwork = a.take<double>((int64_t)small_scratch_doubles(b));
   w.C = a.take<double>(bb);
+  w.C2 = a.take<double>(2 * bb);
+  w.Tb = a.take<double>(bb);
+  w.Mb = a.take<double>(bb);
   w.P = a.take<double>((int64_t)tn_partial_doubles(n, b, b));
   w.theta = a.take<double>(b);
   w.theta_sorted = a.take<double>(b);
@@ -96,6 +106,7 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.perm = a.take<int>(b);
   w.ctrl = a.take<Ctrl>(1);
   w.gersh = a.take<unsigned long long>(1);
+  w.coef_buf = a.take<double>((int64_t)(1 + ops->dim) * ops->ld);
   if (dist && dist->comm) {
     const int64_t hb = (int64_t)b * ops->nx;
     w.send_lo = a.take<double>(hb);
@@ -174,6 +185,40 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
   return SCSF_OK;
 }
 
+// Rayleigh-Ritz with CholQR's second pass folded in.  On entry V[:, k0:b) holds
+// Q1 = F R1^{-1} (first CholQR pass).  With W1 = A Q1, one pass over Q1 gives
+// S2 = Q1^T Q1 and H = Q1^T W1; then R2 = chol(S2), G = R2^{-T} H R2^{-1}
+// (the Rayleigh quotient of Q2 = Q1 R2^{-1}), G = Z Theta Z^T, M = R2^{-1} Z and
+// V <- Q1 M, W <- W1 M (= A V).  Same result as CholQR2 followed by the
+// Rayleigh-Ritz step (Q2 Z = Q1 (R2^{-1} Z)); it saves one n x b pass (the
+// second triangular apply) and fuses two Gram passes into one.  The b x b
+// products are replicated (identical on every rank of a row partition).
+static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int L, double tol, cudaStream_t s) {
+  const int ba = w.b - k0;
+  const int64_t bb = (int64_t)ba * ba;
+  double* Va = w.V + (int64_t)k0 * w.ldv;
+  double* Wa = w.W + (int64_t)k0 * w.ldv;
+  SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
+  SCSF_TRY(gemm_tn_dual(Va, w.ldv, Va, Wa, w.ldv, ba, w.n, w.C2, ba, w.P, s));
+  if (w.comm) SCSF_TRY(w.comm->allreduce_sum(w.C2, (size_t)2 * bb, s));
+  const double* S2 = w.C2;
+  const double* H = w.C2 + bb;
+  SCSF_TRY(chol_inv_impl(S2, ba, ba, w.n_glob, w.Rinv, w.Gwork, w.ctrl, s));
+  SCSF_TRY(gemm_nn_ex(H, ba, ba, ba, w.Rinv, ba, ba, 1.0, 0.0, w.Tb, ba, 1, s));         // T = H R2^{-1}
+  SCSF_TRY(gemm_tn(w.Rinv, ba, ba, w.Tb, ba, ba, ba, 1.0, 1, w.S, ba, w.P, s));           // G = R2^{-T} T (upper)
+  SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
+  SCSF_TRY(gemm_nn_ex(w.Rinv, ba, ba, ba, w.Zs, ba, ba, 1.0, 0.0, w.Mb, ba, 0, s));        // M = R2^{-1} Z
+  SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Va, w.ldv, s));
+  SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
+  SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
+  if (w.comm) {
+    SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
+    SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
+  }
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
+  return SCSF_OK;
+}
+
 // ---- optional phase timers (scsf_set_timing) ----
 static int g_timing = 0;
 int set_timing(int on) {
@@ -235,12 +280,115 @@ static int clear_chol_flag(SolveWS& w, cudaStream_t s) {
   return SCSF_OK;
 }
 
+// ---- CUDA graphs of the outer iteration ----
+// The ~25 launches of one iteration are captured once per (workspace, operator
+// arrays, shape, kL) and replayed with one cudaGraphLaunch: with many chains
+// the host launch rate, not the GPU, bounds throughput otherwise.  The
+// operator's coefficient pointer is part of the key (a new operator of the
+// batch is a new graph; its arrays live in the caller's batch).  Disabled by
+// SCSF_GRAPHS=0, under SCSF_DEBUG_SYNC=1 and for the row-partitioned solve
+// (its loopback collectives synchronise on the host).
+struct GraphKey {
+  const void* V;
+  const void* coef;
+  int64_t n, ldv, ld, dims;
+  int b, kL, degree, L, timing;
+  double tol;
+  bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphKeyHash {
+  size_t operator()(const GraphKey& k) const {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&k);
+    size_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(GraphKey); ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;
+};
+static std::mutex g_graph_mu;
+static std::unordered_map<GraphKey, GraphEntry, GraphKeyHash>* g_graphs = nullptr;
+
+static bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_GRAPHS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1 && !debug_sync();
+}
+
+template <class F>
+static int graph_run(const GraphKey& key0, F&& body, cudaStream_t s) {
+  GraphKey key;
+  memset(&key, 0, sizeof(key));                        // padding bytes take part in the hash / compare
+  key.V = key0.V; key.coef = key0.coef; key.n = key0.n; key.ldv = key0.ldv; key.ld = key0.ld;
+  key.dims = key0.dims; key.b = key0.b; key.kL = key0.kL; key.degree = key0.degree; key.L = key0.L;
+  key.timing = key0.timing; key.tol = key0.tol;
+  GraphEntry e;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (!g_graphs) g_graphs = new std::unordered_map<GraphKey, GraphEntry, GraphKeyHash>();
+    auto it = g_graphs->find(key);
+    if (it != g_graphs->end()) e = it->second;
+  }
+  if (!e.exec) {
+    SCSF_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    set_capturing(true);
+    const int r = body();
+    set_capturing(false);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (r != SCSF_OK) {
+      if (g) cudaGraphDestroy(g);
+      return r;
+    }
+    if (ce != cudaSuccess) {
+      set_error("graph capture failed: %s", cudaGetErrorString(ce));
+      return SCSF_ERR_DEVICE;
+    }
+    size_t nn = 0;
+    SCSF_CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) SCSF_CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      SCSF_CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
+      e.kernels += (t == cudaGraphNodeTypeKernel);
+    }
+    SCSF_CUDA_CHECK(cudaGraphInstantiate(&e.exec, g, 0));
+    cudaGraphDestroy(g);
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graphs->size() > 20000) g_graphs->clear();   // bound the cache (execs are leaked, not freed mid-use)
+    g_graphs->emplace(key, e);
+  }
+  SCSF_CUDA_CHECK(cudaGraphLaunch(e.exec, s));
+  count_launch(e.kernels);
+  return SCSF_OK;
+}
+
 // Solve operator `op`.  warm: V already holds the initial b-block (orthonormal).
 // On return w.V holds the final block sorted ascending with the sign convention,
 // w.theta_sorted the Ritz values.
-int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double tol, int max_iter,
+int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, double tol, int max_iter,
                bool warm, bool orthonormalize, uint64_t seed, SolveWS& w, scsf_stats* st, cudaStream_t s) {
   const int b = L + nex;
+  const bool graphs = graphs_enabled() && !w.comm && s != nullptr && !g_timing;
+  // With graphs, the operator's arrays are first copied into the chain's own
+  // buffer, so every captured iteration is independent of the operator index.
+  scsf_ops opl = *ops_in;
+  int op = op_in;
+  if (graphs) {
+    const size_t per = (size_t)(1 + ops_in->dim) * ops_in->ld;
+    SCSF_CUDA_CHECK(cudaMemcpyAsync(w.coef_buf, ops_in->coef + (int64_t)op_in * per, per * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+    opl.coef = w.coef_buf;
+    opl.n_ops = 1;
+    op = 0;
+  }
+  const scsf_ops* ops = &opl;
   int64_t spmm_cols = 0;
   int filter_steps = 0, iters = 0;
   double filter_bytes = 0.0;
@@ -260,10 +408,11 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
   SCSF_TRY(read_ctrl(w, h, s));
   int kL = h.kL;
   int fallbacks = 0;
-  while (kL < L && iters < max_iter && !(h.nonfinite & 1)) {
-    ++iters;
-    const int ba = b - kL;
-    double* y[3] = {w.V + (int64_t)kL * w.ldv, w.T1 + (int64_t)kL * w.ldv, w.T2 + (int64_t)kL * w.ldv};
+  // One outer iteration (steps 1-6) as device work only; replayed from a CUDA graph
+  // keyed by kL (every pointer and shape of the iteration is a function of kL).
+  auto iteration = [&](int kLc) -> int {
+    const int ba = b - kLc;
+    double* y[3] = {w.V + (int64_t)kLc * w.ldv, w.T1 + (int64_t)kLc * w.ldv, w.T2 + (int64_t)kLc * w.ldv};
     // 1. Chebyshev filter (Alg. 1) on the active block
     SCSF_TRY(tm.mark(0, s));
     double* F;
@@ -277,26 +426,48 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
       F = y[degree % 3];
     }
     SCSF_TRY(tm.mark(1, s));
+    // 2. block classical Gram-Schmidt, twice, against the locked vectors
+    if (kLc > 0) {
+      for (int rep = 0; rep < 2; ++rep) {
+        SCSF_TRY(gram(w, w.V, kLc, F, ba, 0, w.C, s));
+        SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kLc, w.C, kLc, ba, -1.0, 1.0, F, w.ldv, s));
+      }
+    }
+    // 3. CholQR, first pass (lands the block in V's active columns)
+    SCSF_TRY(clear_chol_flag(w, s));
+    SCSF_TRY(cholqr_pass(w, F, y[0], ba, s));
+    SCSF_TRY(tm.mark(2, s));
+    // 4.-6. CholQR's second pass folded into Rayleigh-Ritz, residuals, locking
+    SCSF_TRY(rayleigh_ritz_q1(ops, op, w, kLc, L, tol, s));
+    SCSF_TRY(tm.mark(3, s));
+    return SCSF_OK;
+  };
+  while (kL < L && iters < max_iter && !(h.nonfinite & 1)) {
+    ++iters;
+    const int ba = b - kL;
+    if (graphs) {
+      GraphKey key{};
+      key.V = w.V;
+      key.coef = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+      key.n = w.n;
+      key.ldv = w.ldv;
+      key.ld = ops->ld;
+      key.b = b;
+      key.kL = kL;
+      key.degree = degree;
+      key.L = L;
+      key.timing = tm.on ? 1 : 0;
+      key.dims = ops->nx + 65536LL * (ops->ny + 65536LL * (ops->nz + 65536LL * ops->dim));
+      key.tol = tol;
+      SCSF_TRY(graph_run(key, [&]() { return iteration(kL); }, s));
+    } else {
+      SCSF_TRY(iteration(kL));
+    }
     // algorithmic bytes: first step reads Y0 + writes Y1, later steps read Y_s, Y_{s-1}
     // and write Y_{s+1}; one pass over the coefficient arrays per step
     filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * ba * (degree - 1) + coef_bytes * degree;
     filter_steps += degree;
-    spmm_cols += (int64_t)degree * ba;
-    // 2. block classical Gram-Schmidt, twice, against the locked vectors
-    if (kL > 0) {
-      for (int rep = 0; rep < 2; ++rep) {
-        SCSF_TRY(gram(w, w.V, kL, F, ba, 0, w.C, s));
-        SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kL, w.C, kL, ba, -1.0, 1.0, F, w.ldv, s));
-      }
-    }
-    // 3. CholQR2 (second pass lands the block in V's active columns)
-    SCSF_TRY(clear_chol_flag(w, s));
-    SCSF_TRY(cholqr_pass(w, F, F, ba, s));
-    SCSF_TRY(cholqr_pass(w, F, y[0], ba, s));
-    SCSF_TRY(tm.mark(2, s));
-    // 4.-6. Rayleigh-Ritz, residuals, locking
-    SCSF_TRY(rayleigh_ritz(ops, op, w, kL, L, tol, spmm_cols, s));
-    SCSF_TRY(tm.mark(3, s));
+    spmm_cols += (int64_t)degree * ba + ba;
     SCSF_TRY(read_ctrl(w, h, s));
     SCSF_TRY(tm.accumulate());
     if (h.chol_fail) {
@@ -304,7 +475,7 @@ int solve_core(const scsf_ops* ops, int op, int L, int nex, int degree, double t
       ++fallbacks;
       SCSF_CUDA_CHECK(cudaMemcpyAsync(&w.ctrl->kL, &kL, sizeof(int32_t), cudaMemcpyHostToDevice, s));
       SCSF_TRY(clear_chol_flag(w, s));
-      SCSF_TRY(cholqr_pass(w, y[0], y[0], ba, s));
+      SCSF_TRY(cholqr_pass(w, w.V + (int64_t)kL * w.ldv, w.V + (int64_t)kL * w.ldv, ba, s));
       SCSF_TRY(rayleigh_ritz(ops, op, w, kL, L, tol, spmm_cols, s));
       SCSF_TRY(read_ctrl(w, h, s));
     }

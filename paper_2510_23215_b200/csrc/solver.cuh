@@ -20,10 +20,12 @@ struct SolveWS {
   int nx = 0;
   double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;  // [b][nx] halos
   double *colbuf = nullptr, *colgath = nullptr;                        // sign convention (3 b, world 3 b)
+  double* coef_buf = nullptr;                                          // this operator's arrays (graph replay)
   int b = 0;
   double *V = nullptr, *W = nullptr, *T1 = nullptr, *T2 = nullptr;   // n x b blocks (ld ldv)
   double *S = nullptr, *Rinv = nullptr, *Zs = nullptr, *Zwork = nullptr, *Gwork = nullptr;  // b x b
   double *C = nullptr, *P = nullptr;                                   // projections, split-K partials
+  double *C2 = nullptr, *Tb = nullptr, *Mb = nullptr;                  // [S2 | H] (b x 2b), b x b products
   double *theta = nullptr, *theta_sorted = nullptr, *res = nullptr, *wn = nullptr, *rel = nullptr;
   double* fp = nullptr;                                                // filter (lambda, c, e)
   int* perm = nullptr;
