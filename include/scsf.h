@@ -305,6 +305,10 @@ const char* scsf_last_error(void);   /* thread-local message for the last non-OK
 int scsf_abi_version(void);          /* SCSF_ABI_VERSION                                */
 int64_t scsf_launch_count(void);     /* kernels launched by this process so far         */
 int scsf_set_timing(int32_t on);     /* enable per-phase CUDA-event timers; returns the old state */
+/* which Alg. 1 kernel the solver uses for these operators: 2 = cluster-resident
+ * whole filter (k_filter_cl), 1 = single-CTA resident (k_filter_res2d), 0 = one
+ * streaming launch per step (k_stencil_v4); -1 = invalid ops */
+int scsf_filter_kind(const scsf_ops* ops);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,7 @@ int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double*
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
                  int ncols, const double* fp, int step, cudaStream_t s);
 bool filter_resident_ok(const scsf_ops* ops);
+int filter_kind(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
                          const double* fp, int m, cudaStream_t s);
 
@@ -113,6 +114,10 @@ const char* scsf_last_error(void) { return g_err; }
 int scsf_abi_version(void) { return SCSF_ABI_VERSION; }
 int64_t scsf_launch_count(void) { return g_launches.load(); }
 int scsf_set_timing(int32_t on) { return set_timing(on); }
+int scsf_filter_kind(const scsf_ops* ops) {
+  if (check_ops(ops) != SCSF_OK) return -1;
+  return filter_kind(ops);
+}
 
 size_t scsf_sort_workspace_bytes(int32_t N, int32_t dim, int32_t p, int32_t F, int32_t p0) {
   if (N < 1 || (dim != 2 && dim != 3) || p < 1 || F < 1 || p0 < 1) return 0;

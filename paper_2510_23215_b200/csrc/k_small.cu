@@ -17,6 +17,8 @@
 //  finalize     ascending sort of the b Ritz pairs + sign convention (R21).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace scsf {
 
 // Newton-refined fp64 reciprocal / reciprocal square root for normal, finite
@@ -545,8 +547,16 @@ template <int LOGB>
 __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__ Gin, int64_t ldg, int b,
                                                       double2* __restrict__ rec, int* __restrict__ recm,
                                                       int* __restrict__ nrec_out, double* __restrict__ theta_out,
-                                                      int* __restrict__ rank_out, int max_sweeps, Ctrl* ctrl) {
+                                                      int* __restrict__ rank_out, int max_sweeps, Ctrl* ctrl,
+                                                      int64_t gstride, int match_diag) {
   constexpr int B = 1 << LOGB;
+  // batch (block Jacobi): CTA z works on the z-th diagonal sub-matrix and its own record slots
+  Gin += (int64_t)blockIdx.x * gstride;
+  rec += (int64_t)blockIdx.x * JREC_SWEEPS * 128 * 64;
+  recm += blockIdx.x * JREC_SWEEPS * 128;
+  nrec_out += blockIdx.x;
+  theta_out += (int64_t)blockIdx.x * b;
+  rank_out += (int64_t)blockIdx.x * b;
   constexpr int GP = B + 1;
   constexpr int H2 = B / 2;
   extern __shared__ double G[];                     // [B][GP], upper triangle used
@@ -566,6 +576,18 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
       G[i * GP + j] = v;
       if (i == j) dmax = fmax(dmax, fabs(v));
     }
+  }
+  // block Jacobi: the k-th smallest eigenvalue goes to the position of the k-th smallest
+  // initial diagonal entry (Q close to the identity; sorted sub-solves make block Jacobi cycle)
+  __shared__ int posr[B];
+  if (match_diag && tid < b) {
+    const double v = Gin[tid + (int64_t)tid * ldg];
+    int rk = 0;
+    for (int j = 0; j < b; ++j) {
+      const double u = Gin[j + (int64_t)j * ldg];
+      rk += (u < v) || (u == v && j < tid);
+    }
+    posr[rk] = tid;
   }
   dmax = warp_max(dmax);
   if (lane == 0) red[warp] = dmax;
@@ -665,10 +687,11 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
   if (tid == 0) {
     *nrec_out = nrec;
     if (ctrl) {
-      if (sweep >= max_sweeps || sweep >= JREC_SWEEPS) ctrl->nonfinite |= 2;
-      ctrl->pad[0] += sweep;
+      if (sweep >= max_sweeps || sweep >= JREC_SWEEPS) atomicOr(&ctrl->nonfinite, 2);
+      atomicAdd(&ctrl->pad[0], sweep);
     }
   }
+  __syncthreads();
   if (tid < b) {
     const double v = G[tid * GP + tid];
     int rk = 0;
@@ -676,6 +699,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
       const double w = G[j * GP + j];
       rk += (w < v) || (w == v && j < tid);
     }
+    if (match_diag) rk = posr[rk];
     rank_out[tid] = rk;
     theta_out[rk] = v;
   }
@@ -695,6 +719,11 @@ template <int LOGB>
 __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restrict__ rec, const int* __restrict__ recm,
                                                         const int* __restrict__ nrec_p, const int* __restrict__ rank,
                                                         int b, double* __restrict__ Zout) {
+  rec += (int64_t)blockIdx.y * JREC_SWEEPS * 128 * 64;      // batch: sub-problem blockIdx.y
+  recm += blockIdx.y * JREC_SWEEPS * 128;
+  nrec_p += blockIdx.y;
+  rank += (int64_t)blockIdx.y * b;
+  Zout += (int64_t)blockIdx.y * b * b;
   constexpr int B = 1 << LOGB;
   constexpr int H2 = B / 2;
   constexpr int R = 16;
@@ -1034,11 +1063,21 @@ static int chol_rec(const double* S, int64_t lds, const double* T, int64_t ldt, 
   return SCSF_OK;
 }
 
+size_t blockjac_scratch_doubles(int b);
+int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* jscratch, double* theta,
+                  double* Zout, Ctrl* ctrl, cudaStream_t s);
+static size_t jac_record_doubles(int b) {
+  const int nbatch = b <= 128 ? 1 : (b + 127) / 128;
+  return (size_t)nbatch * (JREC_SWEEPS * 128 * 64 * 2 + JREC_SWEEPS * 128) + 4096;
+}
+
 size_t small_scratch_doubles(int b) {
   // chol_rec: per level 3 b1 b2 + 2 b2^2 (+ the materialised S22 - T22 and its own level);
   // jacobi (b <= 128): the rotation record (JREC_SWEEPS x 127 rounds x 64 pairs of (c, s)) + indices
   const size_t chol = (size_t)8 * b * b + 4096;
-  const size_t jac = (size_t)JREC_SWEEPS * 128 * 64 * 2 + (size_t)JREC_SWEEPS * 128 + 1024;
+  const int nbatch = b <= 128 ? 1 : (b + 127) / 128;   // block Jacobi: up to 3 sub-problems at once
+  const size_t jac = (size_t)nbatch * (JREC_SWEEPS * 128 * 64 * 2 + JREC_SWEEPS * 128) + 4096 +
+                     (b > 128 ? blockjac_scratch_doubles(b) : 0);
   return chol > jac ? chol : jac;
 }
 
@@ -1054,17 +1093,28 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
 
 template <int LOGB>
 static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scratch, double* theta, double* Zout,
-                               Ctrl* ctrl, cudaStream_t s) {
+                               Ctrl* ctrl, cudaStream_t s, int batch = 1, int64_t gstride = 0, int match = 0) {
   constexpr int B = 1 << LOGB;
   double2* rec = reinterpret_cast<double2*>(scratch);
-  int* recm = reinterpret_cast<int*>(scratch + (size_t)JREC_SWEEPS * 128 * 64 * 2);
-  int* nrec = recm + JREC_SWEEPS * 128;
+  int* recm = reinterpret_cast<int*>(scratch + (size_t)batch * JREC_SWEEPS * 128 * 64 * 2);
+  int* nrec = recm + batch * JREC_SWEEPS * 128;
   int* rank = nrec + 32;
-  k_jacobi_g<LOGB><<<1, 1024, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank, 40, ctrl);
+  k_jacobi_g<LOGB><<<batch, 1024, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank, 40,
+                                                                     ctrl, gstride, match);
   SCSF_LAUNCH_CHECK();
-  k_jacobi_z<LOGB><<<ceil_div(b, 16), 8 * B, 0, s>>>(rec, recm, nrec, rank, b, Zout);
+  k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), 8 * B, 0, s>>>(rec, recm, nrec, rank, b, Zout);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
+}
+
+// batched: `batch` diagonal sub-matrices of G (size bs, starting every gstride elements), Q[z] = Zout + z bs^2
+int jacobi_batched_impl(const double* G, int64_t ldg, int bs, int batch, int64_t gstride, double* scratch,
+                        double* theta, double* Q, Ctrl* ctrl, cudaStream_t s) {
+  if (bs <= 32) return jacobi_split_launch<5>(G, ldg, bs, scratch, theta, Q, ctrl, s, batch, gstride, 1);
+  if (bs <= 64) return jacobi_split_launch<6>(G, ldg, bs, scratch, theta, Q, ctrl, s, batch, gstride, 1);
+  if (bs <= 128) return jacobi_split_launch<7>(G, ldg, bs, scratch, theta, Q, ctrl, s, batch, gstride, 1);
+  set_error("jacobi_batched: sub-problem %d > 128", bs);
+  return SCSF_ERR_NOT_IMPLEMENTED;
 }
 
 // scratchG: >= small_scratch_doubles(b) doubles; Z: b*b doubles (global fallback only)
@@ -1078,6 +1128,8 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
   if (b <= 32) return jacobi_split_launch<5>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
   if (b <= 64) return jacobi_split_launch<6>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
   if (b <= 128) return jacobi_split_launch<7>(G, ldg, b, scratchG, theta, Zout, ctrl, s);
+  if (!(getenv("SCSF_PLAIN_JACOBI") && getenv("SCSF_PLAIN_JACOBI")[0] == '1'))
+    return blockjac_impl(G, ldg, b, scratchG + jac_record_doubles(b), scratchG, theta, Zout, ctrl, s);
   if (b <= JAC_SMEM_MAX_B)
     k_jacobi<true><<<1, 1024, jac_smem(b), s>>>(G, ldg, b, scratchG, Z, theta, Zout, 40, ctrl);
   else

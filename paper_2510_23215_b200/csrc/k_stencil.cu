@@ -446,11 +446,13 @@ __global__ void __launch_bounds__(RQ_T, 1) k_filter_res2d_q(const double* __rest
 // All m steps of Alg. 1 for CB columns on a thread-block cluster of CS CTAs:
 // CTA r of the cluster owns grid rows [r R, r R + R) (R = ceil(ny / CS), even)
 // of CB consecutive columns.  Everything the recurrence touches stays on chip:
-//  - a thread owns a vertical pair of quads (rows 2p, 2p+1, 4 consecutive x):
-//    their coefficients (diag, cx, cy, cx(k-1), and cy(k-nx) of the lower
-//    quad; the upper quad's cy(k-nx) is the lower quad's cy) live in
-//    registers, loaded once per filter and shared by the CB columns; the pair
-//    shares its vertical neighbours (4 quad loads per 2 output quads);
+//  - a thread owns a 2 x 2 patch: rows 2p, 2p+1 at x = 2q, 2q+1.  Lanes run
+//    along x, so every shared access is a 16-byte vector at a 16-byte stride
+//    (bank-conflict free) and the x-neighbours come from the adjacent lanes by
+//    shuffle (lane 0 / 31 read shared memory; across a row end the coupling cx
+//    is 0).  The patch's coefficients (diag, cx, cy, cx(k-1), cy(k-nx)) live
+//    in registers, loaded once per filter and shared by the CB columns; the
+//    upper row's cy(k-nx) is the lower row's cy;
 //  - Y_s and Y_{s-1} of each column live in two shared buffers of R + 2 rows
 //    (one ghost row each side); Y_{s-1} is read from the target buffer
 //    (written two steps ago), so no vector state survives a step in registers;
@@ -460,12 +462,29 @@ __global__ void __launch_bounds__(RQ_T, 1) k_filter_res2d_q(const double* __rest
 //    rows stay zero.
 // HBM traffic per filter and column: read Y_0, write Y_m (16 n B) plus the
 // coefficient arrays once per CB columns.  Bound: shared-memory bandwidth
-// (~144 B per quad per step) and the cluster barrier (amortised over CB).
-constexpr int CL_T = 512;                        // threads per CTA (<= 128 registers each)
-constexpr int CL_MAXQ = 2 * CL_T;                // quads per CTA
+// (~32 B per point per step) and the cluster barrier (amortised over CB).
+constexpr int CL_T = 768;                        // max threads per CTA (<= 85 registers each)
+constexpr int CL_MAXP = CL_T;                    // 2 x 2 patches per CTA
 
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// 32-bit shared-memory accesses (volatile: they must not move across the cluster barrier)
+__device__ __forceinline__ double2 lds2a(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds1a(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts2a(unsigned a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
 template <int CS, int CB>
@@ -474,143 +493,142 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
+  __shared__ double sa[128], sb[128];                      // per-step scalars (m <= 128)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int j0 = blockIdx.y * CB, tid = threadIdx.x;
+  const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
   const int R = ((ny + CS - 1) / CS + 1) & ~1;
   const int row0 = rank * R;
   const int rows = max(0, min(R, ny - row0));
-  const int qrow = nx >> 2;
-  const int npairs = ((rows + 1) >> 1) * qrow;
+  const int hx = nx >> 1;                                  // 2-point segments per row
+  const int npatch = ((rows + 1) >> 1) * hx;
   const int pitch = (R + 2) * nx;                          // one buffer of one column
   const int n = nx * ny;
-  const double lam = fp[0], c = fp[1], e = fp[2];
-  const double s1 = e / (lam - c);
+  const int ncb = min(CB, ncols - j0);                     // columns of this CTA (uniform)
+  const double c = fp[1];
+  if (tid == 0) {                                          // Alg. 1 scalars, same operation sequence as step_scalars()
+    const double lam = fp[0], e = fp[2];
+    const double s1 = e / (lam - c);
+    double sig = s1;
+    sa[0] = s1 / e;
+    sb[0] = 0.0;
+    for (int st = 1; st < m && st < 128; ++st) {
+      const double sn = 1.0 / (2.0 / s1 - sig);
+      sa[st] = 2.0 * sn / e;
+      sb[st] = -sn * sig;
+      sig = sn;
+    }
+  }
   const bool has_lo = rank > 0;
   const bool has_hi = (rank + 1 < CS) && (row0 + R < ny);
   double* lo_buf = has_lo ? cluster.map_shared_rank(cbuf, rank - 1) : nullptr;   // CTA below
   double* hi_buf = has_hi ? cluster.map_shared_rank(cbuf, rank + 1) : nullptr;   // CTA above
-  // Dirichlet ghost rows (both buffers, every column) are zero
-  for (int i = tid; i < CB * 2 * nx; i += CL_T) {
-    const int col = i / (2 * nx), r = i % (2 * nx);
-    double* base = cbuf + (size_t)(2 * col + r / nx) * pitch;
-    if (!has_lo) base[r % nx] = 0.0;
-    if (!has_hi) base[(rows + 1) * nx + r % nx] = 0.0;
-  }
-  cluster_barrier();                                       // every CTA of the cluster is running
-  // Y_0: own rows into buffer 0, boundary rows also into the neighbours' ghost rows
-  for (int cc = 0; cc < CB; ++cc) {
-    const int j = j0 + cc;
-    if (j >= ncols) break;
-    const double* x0 = X + (int64_t)j * ldv + (int64_t)row0 * nx;
+  // all buffers zero: Dirichlet ghost rows, and Y_{-1} = 0 for the first step's (bco = 0) term
+  for (int i = tid; i < CB * pitch; i += nthr) sts2(cbuf + 2 * i, make_double2(0.0, 0.0));
+  cluster_barrier();                                       // every CTA of the cluster is running and zeroed
+  for (int cc = 0; cc < ncb; ++cc) {                       // Y_0 (own rows; boundary rows also to the neighbours)
+    const double* x0 = X + (int64_t)(j0 + cc) * ldv + (int64_t)row0 * nx;
     double* b0 = cbuf + (size_t)(2 * cc) * pitch;
-    for (int q = tid; q < rows * qrow; q += CL_T) {
-      const double4 v = ldg4_nc(x0 + 4 * q);
-      sts4(b0 + nx + 4 * q, v);
-      const int lr = q / qrow, xq = 4 * (q % qrow);
-      if (lr == 0 && lo_buf) sts4(lo_buf + (size_t)(2 * cc) * pitch + (R + 1) * nx + xq, v);
-      if (lr == rows - 1 && hi_buf) sts4(hi_buf + (size_t)(2 * cc) * pitch + xq, v);
+    for (int q = tid; q < rows * hx; q += nthr) {
+      const double2 v = *reinterpret_cast<const double2*>(x0 + 2 * q);
+      sts2(b0 + nx + 2 * q, v);
+      const int lr = q / hx, xq = 2 * (q % hx);
+      if (lr == 0 && lo_buf) sts2(lo_buf + (size_t)(2 * cc) * pitch + (R + 1) * nx + xq, v);
+      if (lr == rows - 1 && hi_buf) sts2(hi_buf + (size_t)(2 * cc) * pitch + xq, v);
     }
   }
-  // this thread's pair: local rows lr0, lr0 + 1; x = xq
-  const bool act = tid < npairs;
-  const int lr0 = 2 * (tid / qrow), xq = 4 * (tid % qrow);
+  // this thread's patch: local rows lr0, lr0 + 1; x = xq, xq + 1.  Inactive threads compute on
+  // a valid patch (the last one) and store nothing, so the step loop has no divergent branches.
+  const bool act = tid < npatch;
+  const int pt = min(tid, max(npatch - 1, 0));
+  const int lr0 = 2 * (pt / hx), xq = 2 * (pt % hx);
   const bool up_ok = act && (lr0 + 1 < rows);
   const int g0 = (row0 + lr0) * nx + xq;
-  const double4 z4 = make_double4(0, 0, 0, 0);
-  double4 dg0 = z4, dg1 = z4, cxp0 = z4, cxp1 = z4, cyp0 = z4, cyp1 = z4, cym0 = z4;
+  const double2 z2 = make_double2(0, 0);
+  double2 dg0 = z2, dg1 = z2, cxp0 = z2, cxp1 = z2, cyp0 = z2, cyp1 = z2, cym0 = z2;
   double cxm0 = 0.0, cxm1 = 0.0;
-  if (act) {
-    dg0 = ldg4_nc(cf + g0);
-    cxp0 = ldg4_nc(cf + ldc + g0);
+  if (npatch > 0) {
+    dg0 = *reinterpret_cast<const double2*>(cf + g0);
+    cxp0 = *reinterpret_cast<const double2*>(cf + ldc + g0);
     cxm0 = (g0 >= 1) ? __ldg(cf + ldc + g0 - 1) : 0.0;
-    cyp0 = ldg4_nc(cf + 2 * ldc + g0);
-    cym0 = (g0 >= nx) ? ldg4_nc(cf + 2 * ldc + g0 - nx) : z4;
-    dg0.x -= c; dg0.y -= c; dg0.z -= c; dg0.w -= c;
-  }
-  if (up_ok) {
-    const int g1 = g0 + nx;
-    dg1 = ldg4_nc(cf + g1);
-    cxp1 = ldg4_nc(cf + ldc + g1);
-    cxm1 = __ldg(cf + ldc + g1 - 1);
-    cyp1 = ldg4_nc(cf + 2 * ldc + g1);
-    dg1.x -= c; dg1.y -= c; dg1.z -= c; dg1.w -= c;
-  }
-  // boundary-row destinations in the neighbours (local row 0 -> below's top ghost; last row -> above's bottom ghost)
-  const bool push_lo0 = act && lo_buf && lr0 == 0;
-  const bool push_hi0 = act && hi_buf && lr0 == rows - 1;          // lower quad is the last row (rows odd)
-  const bool push_hi1 = up_ok && hi_buf && lr0 + 1 == rows - 1;    // upper quad is the last row
-  cluster_barrier();
-  double sig = s1;
-  const int l0 = (lr0 + 1) * nx + xq;                      // local index of the lower quad (ghost row 0 first)
-  for (int st = 0; st < m; ++st) {
-    double a, bco;
-    if (st == 0) {
-      a = s1 / e;
-      bco = 0.0;
-    } else {                                               // same operation sequence as step_scalars()
-      const double sn = 1.0 / (2.0 / s1 - sig);
-      a = 2.0 * sn / e;
-      bco = -sn * sig;
-      sig = sn;
+    cyp0 = *reinterpret_cast<const double2*>(cf + 2 * ldc + g0);
+    cym0 = (g0 >= nx) ? *reinterpret_cast<const double2*>(cf + 2 * ldc + g0 - nx) : z2;
+    dg0.x -= c; dg0.y -= c;
+    if (lr0 + 1 < rows) {
+      const int g1 = g0 + nx;
+      dg1 = *reinterpret_cast<const double2*>(cf + g1);
+      cxp1 = *reinterpret_cast<const double2*>(cf + ldc + g1);
+      cxm1 = __ldg(cf + ldc + g1 - 1);
+      cyp1 = *reinterpret_cast<const double2*>(cf + 2 * ldc + g1);
+      dg1.x -= c; dg1.y -= c;
     }
-    if (act) {
+  }
+  const bool push_lo0 = act && lo_buf && lr0 == 0;
+  const bool push_hi0 = act && hi_buf && lr0 == rows - 1;          // lower row is the last row (rows odd)
+  const bool push_hi1 = up_ok && hi_buf && lr0 + 1 == rows - 1;    // upper row is the last row
+  const bool fix_l = (lane == 0) || (xq == 0);                     // left neighbour not in the lane below
+  const bool fix_r = (lane == 31) || (xq + 2 == nx) || (tid + 1 >= npatch);
+  // 32-bit shared addresses of the patch in both buffers of every column
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(cbuf);
+  const int l0 = (lr0 + 1) * nx + xq;                      // local index of the lower row (ghost row 0 first)
+  const unsigned nx8 = 8u * nx;
+  const unsigned up8 = up_ok ? 2u * nx8 : nx8;             // upper neighbour of the upper row (dummy if absent)
+  unsigned acur[CB], anxt[CB];
 #pragma unroll
-      for (int cc = 0; cc < CB; ++cc) {
-        if (j0 + cc >= ncols) break;
-        const size_t cur_off = (size_t)(2 * cc + (st & 1)) * pitch;
-        const size_t nxt_off = (size_t)(2 * cc + ((st + 1) & 1)) * pitch;
-        const double* cur = cbuf + cur_off;
-        double* nxt = cbuf + nxt_off;
-        const double4 xd = lds4(cur + l0 - nx);
-        const double4 xa = lds4(cur + l0);
-        const double4 xb = lds4(cur + l0 + nx);
-        const double xal = cur[l0 - 1], xar = cur[l0 + 4];
-        double4 v;
+  for (int cc = 0; cc < CB; ++cc) {
+    acur[cc] = sbase + 8u * (unsigned)((2 * cc) * pitch + l0);
+    anxt[cc] = sbase + 8u * (unsigned)((2 * cc + 1) * pitch + l0);
+  }
+  cluster_barrier();                                       // also publishes sa / sb
+  for (int st = 0; st < m; ++st) {
+    const double a = sa[st], bco = sb[st];
+    const int nofs = ((st + 1) & 1) ? pitch : 0;            // target buffer of the DSMEM pushes
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+      if (cc < ncb) {                                      // uniform across the CTA
+        const unsigned ca = acur[cc], na = anxt[cc];
+        const double2 xd = lds2a(ca - nx8);
+        const double2 xa = lds2a(ca);
+        const double2 xb = lds2a(ca + nx8);
+        const double2 xu = lds2a(ca + up8);
+        double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
+        double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
+        if (fix_l) {
+          xal = lds1a(ca - 8u);
+          xbl = lds1a(ca + nx8 - 8u);
+        }
+        if (fix_r) {
+          xar = lds1a(ca + 16u);
+          xbr = lds1a(ca + nx8 + 16u);
+        }
+        double2 v, u;
         v.x = fma(dg0.x, xa.x, fma(cxp0.x, xa.y, fma(cxm0, xal, fma(cyp0.x, xb.x, cym0.x * xd.x))));
-        v.y = fma(dg0.y, xa.y, fma(cxp0.y, xa.z, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
-        v.z = fma(dg0.z, xa.z, fma(cxp0.z, xa.w, fma(cxp0.y, xa.y, fma(cyp0.z, xb.z, cym0.z * xd.z))));
-        v.w = fma(dg0.w, xa.w, fma(cxp0.w, xar, fma(cxp0.z, xa.z, fma(cyp0.w, xb.w, cym0.w * xd.w))));
-        if (st > 0) {
-          const double4 p = lds4(nxt + l0);
-          v.x = fma(bco, p.x, a * v.x); v.y = fma(bco, p.y, a * v.y);
-          v.z = fma(bco, p.z, a * v.z); v.w = fma(bco, p.w, a * v.w);
-        } else {
-          v.x *= a; v.y *= a; v.z *= a; v.w *= a;
-        }
-        if (up_ok) {
-          const double4 xu = lds4(cur + l0 + 2 * nx);
-          const double xbl = cur[l0 + nx - 1], xbr = cur[l0 + nx + 4];
-          double4 u;
-          u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
-          u.y = fma(dg1.y, xb.y, fma(cxp1.y, xb.z, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
-          u.z = fma(dg1.z, xb.z, fma(cxp1.z, xb.w, fma(cxp1.y, xb.y, fma(cyp1.z, xu.z, cyp0.z * xa.z))));
-          u.w = fma(dg1.w, xb.w, fma(cxp1.w, xbr, fma(cxp1.z, xb.z, fma(cyp1.w, xu.w, cyp0.w * xa.w))));
-          if (st > 0) {
-            const double4 p = lds4(nxt + l0 + nx);
-            u.x = fma(bco, p.x, a * u.x); u.y = fma(bco, p.y, a * u.y);
-            u.z = fma(bco, p.z, a * u.z); u.w = fma(bco, p.w, a * u.w);
-          } else {
-            u.x *= a; u.y *= a; u.z *= a; u.w *= a;
-          }
-          sts4(nxt + l0 + nx, u);
-          if (push_hi1) sts4(hi_buf + nxt_off + xq, u);
-        }
-        sts4(nxt + l0, v);
-        if (push_lo0) sts4(lo_buf + nxt_off + (R + 1) * nx + xq, v);
-        if (push_hi0) sts4(hi_buf + nxt_off + xq, v);
+        v.y = fma(dg0.y, xa.y, fma(cxp0.y, xar, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
+        u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
+        u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
+        // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
+        const double2 p0 = lds2a(na), p1 = lds2a(na + nx8);
+        v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
+        u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
+        if (act) sts2a(na, v);
+        if (up_ok) sts2a(na + nx8, u);
+        const int colofs = 2 * cc * pitch + nofs;
+        if (push_lo0) sts2(lo_buf + colofs + (R + 1) * nx + xq, v);
+        if (push_hi0) sts2(hi_buf + colofs + xq, v);
+        if (push_hi1) sts2(hi_buf + colofs + xq, u);
+        acur[cc] = na;
+        anxt[cc] = ca;
       }
     }
     cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
   }
-  for (int cc = 0; cc < CB; ++cc) {
-    const int j = j0 + cc;
-    if (j >= ncols) break;
+  for (int cc = 0; cc < ncb; ++cc) {
     const double* fin = cbuf + (size_t)(2 * cc + (m & 1)) * pitch;
-    double* out = Out + (int64_t)j * ldv;
-    for (int q = tid; q < rows * qrow; q += CL_T) stg4(out + row0 * nx + 4 * q, lds4(fin + nx + 4 * q));
+    double* out = Out + (int64_t)(j0 + cc) * ldv;
+    for (int q = tid; q < rows * hx; q += nthr)
+      *reinterpret_cast<double2*>(out + row0 * nx + 2 * q) = lds2(fin + nx + 2 * q);
     if (rank == CS - 1)                                    // ld padding of the column
-      for (int k = n + tid; k < (int)ldv; k += CL_T) out[k] = 0.0;
+      for (int k = n + tid; k < (int)ldv; k += nthr) out[k] = 0.0;
   }
 }
 
@@ -771,12 +789,19 @@ int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaSt
 
 static int g_res_attr = 0;
 static int cluster_size_for(const scsf_ops* ops) {
-  if (ops->dim != 2 || ops->nx % 4 != 0) return 0;
-  const int qrow = ops->nx / 4;
+  if (ops->dim != 2 || ops->nx % 2 != 0) return 0;
   for (int cs = 1; cs <= 8; cs *= 2) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
-    if (R * qrow <= CL_MAXQ && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024) return cs;
+    if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024)
+      return cs;
   }
+  return 0;
+}
+
+// 2: cluster-resident (k_filter_cl), 1: single-CTA resident (k_filter_res2d*), 0: per-step streaming
+int filter_kind(const scsf_ops* ops) {
+  if (cluster_size_for(ops) > 0) return 2;
+  if (ops->dim == 2 && (int64_t)ops->nx * ops->ny <= RES_MAX_N) return 1;
   return 0;
 }
 
@@ -833,23 +858,20 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
   if (ncols <= 0) return SCSF_OK;
   const int n = ops->nx * ops->ny;
   const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
-  if (!g_res_attr) {
-    SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * RES_MAX_N * (int)sizeof(double)));
-    SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * 4 * RQ_T * RQ_Q * (int)sizeof(double)));
-    g_res_attr = 1;
-  }
+  SCSF_TRY(stencil_init_attrs());
   const bool quad = (ops->nx % 4 == 0) && (ldv % 4 == 0) && (ops->ld % 4 == 0) && ((uintptr_t)X % 32 == 0) &&
                     ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0);
-  const int cs = quad ? cluster_size_for(ops) : 0;
+  const bool pair = (ops->nx % 2 == 0) && (ldv % 2 == 0) && (ops->ld % 2 == 0) && ((uintptr_t)X % 16 == 0) &&
+                    ((uintptr_t)Out % 16 == 0) && ((uintptr_t)cf % 16 == 0);
+  const int cs = pair ? cluster_size_for(ops) : 0;
   if (cs > 0) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
     const int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
+    const int thr = (int)round_up((int64_t)(R / 2) * (ops->nx / 2), 32);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, ceil_div(ncols, cb), 1);
-    cfg.blockDim = dim3(CL_T, 1, 1);
+    cfg.blockDim = dim3(thr, 1, 1);
     cfg.dynamicSmemBytes = per_col * cb;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

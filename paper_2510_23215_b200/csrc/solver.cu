@@ -209,7 +209,8 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
   SCSF_TRY(gemm_nn_ex(w.Rinv, ba, ba, ba, w.Zs, ba, ba, 1.0, 0.0, w.Mb, ba, 0, s));        // M = R2^{-1} Z
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Va, w.ldv, s));
-  SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
+  // W = A V by one stencil pass (cheaper than the n x b x b product W1 M; only the residuals use it)
+  SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
   SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
   if (w.comm) {
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
@@ -445,7 +446,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   while (kL < L && iters < max_iter && !(h.nonfinite & 1)) {
     ++iters;
     const int ba = b - kL;
-    if (graphs) {
+    if (graphs && ba <= 128) {          // b > 128: the block Jacobi synchronises per sweep (not capturable)
       GraphKey key{};
       key.V = w.V;
       key.coef = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
@@ -467,7 +468,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     // and write Y_{s+1}; one pass over the coefficient arrays per step
     filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * ba * (degree - 1) + coef_bytes * degree;
     filter_steps += degree;
-    spmm_cols += (int64_t)degree * ba + ba;
+    spmm_cols += (int64_t)degree * ba + 2 * ba;
     SCSF_TRY(read_ctrl(w, h, s));
     SCSF_TRY(tm.accumulate());
     if (h.chol_fail) {

@@ -29,6 +29,7 @@ EXPORTED = [
     "scsf_dev_workspace_bytes", "scsf_gemm_tn", "scsf_gemm_nn", "scsf_chol_inv", "scsf_syev_small",
     "scsf_comm_unique_id", "scsf_comm_create", "scsf_comm_create_loopback", "scsf_comm_destroy",
     "scsf_comm_rank", "scsf_slab_rows", "scsf_solve_dist_workspace_bytes", "scsf_solve_queue_dist",
+    "scsf_filter_kind",
 ]
 
 
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_gemm_nn": (ctypes.c_int, [P, I64, I64, I32, P, I64, I32, D, D, P, I64, P]),
         "scsf_chol_inv": (ctypes.c_int, [P, I64, I32, I64, P, P, SZ, P]),
         "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, P, SZ, P]),
+        "scsf_filter_kind": (ctypes.c_int, [OPS]),
         "scsf_comm_unique_id": (ctypes.c_int, [P]),
         "scsf_comm_create": (ctypes.c_int, [I32, I32, P, ctypes.POINTER(P)]),
         "scsf_comm_create_loopback": (ctypes.c_int, [I32, P]),
@@ -144,6 +146,16 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 def launch_count() -> int:
     return int(load_library().scsf_launch_count())
+
+
+FILTER_KERNELS = {2: "k_filter_cl (cluster-resident whole filter, Alg. 1)",
+                  1: "k_filter_res2d (single-CTA resident whole filter, Alg. 1)",
+                  0: "k_stencil_v4 (one streaming launch per filter step, Alg. 1)"}
+
+
+def filter_kind(ops: "Operators") -> int:
+    st = ops.c_struct()
+    return int(load_library().scsf_filter_kind(ctypes.byref(st)))
 
 
 def set_timing(on: bool) -> bool:

@@ -109,7 +109,8 @@ def test_chol_inv_fallback_flag(lib):
 
 
 @pytest.mark.parametrize("b,kind", [(1, "dense"), (2, "dense"), (19, "dense"), (120, "dense"), (120, "warm"),
-                                    (133, "dense"), (160, "dense"), (240, "warm"), (64, "degenerate")])
+                                    (133, "dense"), (160, "dense"), (240, "warm"), (64, "degenerate"),
+                                    (129, "warm"), (240, "dense"), (360, "warm"), (300, "degenerate")])
 def test_syev_small(lib, b, kind):
     import torch
     rng = np.random.default_rng(b)
@@ -130,7 +131,10 @@ def test_syev_small(lib, b, kind):
     Zn = Z.cpu().numpy().T
     w = np.linalg.eigvalsh(G)
     scale = np.abs(w).max()
+    # b > 128 runs the block Jacobi (k_blockjac.cu): each round rotates the whole matrix with
+    # n-long products, so rounding accumulates ~ n eps per round; the bar is the north-star 1e-12
+    tol = 1e-13 if b <= 128 else 1e-12
     assert np.all(np.diff(th) >= 0)
-    assert np.abs(th - w).max() <= 1e-13 * scale
-    assert np.abs(Zn.T @ Zn - np.eye(b)).max() <= 1e-13
-    assert np.abs(G @ Zn - Zn * th).max() <= 1e-13 * scale
+    assert np.abs(th - w).max() <= tol * scale
+    assert np.abs(Zn.T @ Zn - np.eye(b)).max() <= tol
+    assert np.abs(G @ Zn - Zn * th).max() <= tol * scale
