@@ -14,6 +14,8 @@
 //            alias X (in-place rotation).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace scsf {
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -88,13 +90,13 @@ __global__ void __launch_bounds__(128) k_gemm_tn(const double* __restrict__ X, i
 // the 8 warp sums are then added in warp order: a fixed order, so deterministic.
 // Symmetric results (Gram, Rayleigh quotient) are read as upper triangles by their consumers.
 __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ P, int splits, int b1,
-                                                         int b2, double alpha, int upper_cols,
+                                                         int b2, double alpha, int upper, int gw,
                                                          double* __restrict__ C, int64_t ldc) {
   __shared__ double part[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   const int j = blockIdx.y;
-  if (j < upper_cols && (int)blockIdx.x * 32 > j) return;   // tile strictly below the diagonal
+  if (upper && (int)blockIdx.x * 32 > j % gw) return;     // tile strictly below the diagonal (of its group)
   const int64_t stride = (int64_t)b1 * b2;
   double s = 0.0;
   if (i < b1) {
@@ -172,8 +174,9 @@ __global__ void __launch_bounds__(128) k_gemm_nn(const double* __restrict__ X, i
 }
 
 // =====================================================================
-// v2 tiles: 256 threads (8 warps, 2 x 4), 64 x 64 CTA tile, warp tile 32 x 16
-// (4 x 2 DMMA m8n8k4 per k-step), k-chunks of 32 moved by cp.async into a
+// v2 tiles: 128 threads (4 warps, 2 x 2), 64 x 64 CTA tile, warp tile 32 x 32
+// (4 x 4 DMMA m8n8k4 per k-step: 16 independent accumulators per warp, 8
+// fragment loads per 16 DMMA), k-chunks of 32 moved by cp.async into a
 // 2-stage shared-memory ring.  Shared-memory row pitch 36 doubles (= 4 mod 16)
 // makes every fragment load conflict-free per half-warp.
 // =====================================================================
@@ -190,9 +193,10 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int V2_T = 64, V2_KC = 32, V2_P = V2_KC + 4;   // tile, k-chunk, pitch
+constexpr int V2_NT = 128;                                 // threads per CTA
 
 // ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
-__global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
+__global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
                                                   const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
                                                   int64_t kchunk, int upper, int a16, double* __restrict__ P,
                                                   const double* __restrict__ Y2) {
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
   const int T2 = (b2 + V2_T - 1) / V2_T;
   const int grp = Y2 ? (int)blockIdx.y / T2 : 0;
   const int ti = blockIdx.x, tj = Y2 ? (int)blockIdx.y % T2 : (int)blockIdx.y;
-  if (upper && grp == 0 && ti > tj) return;
+  if (upper && ti > tj) return;                     // dual mode: both products upper-triangle
   if (grp) Y = Y2;
   const int i0 = ti * V2_T, j0 = tj * V2_T;
   const int b2tot = Y2 ? 2 * b2 : b2;
@@ -212,14 +216,14 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
   const int64_t kend = min(n, kbeg + kchunk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int nck = (int)((kend - kbeg + V2_KC - 1) / V2_KC);
 
   auto issue = [&](int c, int stage) {
     const int64_t k0 = kbeg + (int64_t)c * V2_KC;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + 256 * q;               // 0..1023
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + V2_NT * q;             // 0..1023
       const int col = idx >> 4, seg = idx & 15;    // 64 columns x 16 16-byte segments
       const int64_t k = k0 + 2 * seg;
       const int rem = (int)max((int64_t)0, min((int64_t)2, kend - k));
@@ -240,11 +244,11 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
     }
   };
 
-  double acc[4][2][2];
+  double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   issue(0, 0);
   cp_commit();
@@ -261,15 +265,15 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
     const double* yb = ys + ((c & 1) * V2_T + wn + g) * V2_P + t;
 #pragma unroll
     for (int kk = 0; kk < V2_KC; kk += 4) {
-      double a[4], b[2];
+      double a[4], b[4];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * V2_P + kk];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[ni] = yb[ni * 8 * V2_P + kk];
+      for (int ni = 0; ni < 4; ++ni) b[ni] = yb[ni * 8 * V2_P + kk];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
     }
     __syncthreads();
   }
@@ -277,7 +281,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
+    for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + 2 * t + e;
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn2(const double* __restrict__ X, 
 // k > last column of the pass are skipped.
 constexpr int NN2_MAX_K = 128;
 
-__global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
+__global__ void __launch_bounds__(V2_NT) k_gemm_nn2(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
                                                   const double* __restrict__ M, int64_t ldm, int b2,
                                                   double alpha, double beta, double* Out, int64_t ldo,
                                                   int tri_upper, int a16) {
@@ -302,14 +306,14 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
   const int64_t r0 = (int64_t)blockIdx.x * V2_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int nck_all = b1r / V2_KC;
   const int rows_here = (int)min((int64_t)V2_T, n - r0);
 
   auto issue_panel = [&](int c) {      // 32 k-columns x 64 rows: 32 x 32 16-byte segments
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + 256 * q;
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + V2_NT * q;
       const int kk = idx >> 5, seg = idx & 31;
       const int k = c * V2_KC + kk;
       const int rr = 2 * seg;
@@ -326,8 +330,8 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
   };
   auto issue_m = [&](int c, int j0, int stage) {   // 64 columns x 32 k (8-byte copies; ldm may be odd)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = tid + 256 * q;               // 0..2047
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + V2_NT * q;             // 0..2047
       const int j = idx >> 5, kk = idx & 31;
       const int k = c * V2_KC + kk;
       const bool ok = (k < b1) && (j0 + j < b2);
@@ -341,11 +345,11 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
     const int nck = tri_upper ? min(nck_all, (min(b2, j0 + V2_T) + V2_KC - 1) / V2_KC) : nck_all;
     // the whole panel is needed before any write: in the first pass load every chunk
     const int ncp = first ? nck_all : 0;
-    double acc[4][2][2];
+    double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     // groups: G_c = {M chunk c, panel chunk c (first pass)}; remaining panel chunks ride on the last group
     for (int c = 0; c < 2 && c < nck; ++c) {
       issue_m(c, j0, c);
@@ -360,15 +364,15 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
       const double* mb = ms + ((c & 1) * V2_T + wn + g) * V2_P + t;
 #pragma unroll
       for (int kk = 0; kk < V2_KC; kk += 4) {
-        double a[4], b[2];
+        double a[4], b[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * (V2_T + 4) + mi * 8];
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = mb[ni * 8 * V2_P + kk];
+        for (int ni = 0; ni < 4; ++ni) b[ni] = mb[ni * 8 * V2_P + kk];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
       __syncthreads();
       if (c + 2 < nck) {
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t r = r0 + wm + mi * 8 + g;
@@ -399,6 +403,18 @@ __global__ void __launch_bounds__(256) k_gemm_nn2(const double* __restrict__ X, 
           }
         }
   }
+}
+
+// A (b x b, ld) <- upper triangle mirrored into the strict lower triangle
+__global__ void k_symm_upper(double* __restrict__ A, int b, int64_t ld) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < b && i > j) A[i + (int64_t)j * ld] = A[j + (int64_t)i * ld];
+}
+
+int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s) {
+  k_symm_upper<<<dim3(ceil_div(b, 128), b), 128, 0, s>>>(A, b, ld);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
 }
 
 // ------------------------------------------------------------------ host ----
@@ -421,10 +437,23 @@ int dense_init_attrs() {
   return SCSF_OK;
 }
 
+// Rows of the reduction dimension per split-K CTA, at least: long k-loops amortise the
+// pipeline prologue and keep the partial-sum traffic small (with many concurrent chains the
+// GPU is full anyway, so per-CTA efficiency beats spreading one product over every SM).
+static int tn_min_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_TN_MIN_ROWS");
+    v = e ? atoi(e) : 512;
+    if (v < 32) v = 32;
+  }
+  return v;
+}
+
 int tn_splits(int64_t n, int b1, int b2) {
   int tiles = ceil_div(b1, TN_BM) * ceil_div(b2, TN_BM);
   int want = max(1, (2 * 148 + tiles - 1) / tiles);
-  int maxs = max(1, ceil_div(n, 128));              // at least 128 rows (4 k-chunks) per split
+  int maxs = max(1, ceil_div(n, tn_min_rows()));
   return min(want, maxs);
 }
 
@@ -448,38 +477,39 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   int splits = tn_splits(n, b1, b2);
   if (upper) {
     const int t = ceil_div(b1, V2_T);
-    splits = min(max(1, ceil_div(n, 128)), max(1, (2 * 148 + t * (t + 1) / 2 - 1) / (t * (t + 1) / 2)));
+    splits = min(max(1, ceil_div(n, tn_min_rows())), max(1, (2 * 148 + t * (t + 1) / 2 - 1) / (t * (t + 1) / 2)));
   }
   int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
   const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
-  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
+  k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b1, 32), b2);
-  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper ? b2 : 0, C, ldc);
+  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper, b2, C, ldc);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
 
-// One pass over X for two products: C[:, 0:b) = X^T Y1 (upper triangle; X == Y1),
-// C[:, b:2b) = X^T Y2 (full).  C is b x 2b (ldc >= b).
+// One pass over X for two symmetric products: C[:, 0:b) = X^T Y1, C[:, b:2b) = X^T Y2,
+// upper triangles only (X^T Y2 symmetric in exact arithmetic: the Rayleigh quotient).
+// C is b x 2b (ldc >= b).
 int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y2, int64_t ldy, int b, int64_t n,
                  double* C, int64_t ldc, double* P, cudaStream_t s) {
   if (b <= 0) return SCSF_OK;
   SCSF_TRY(dense_init_attrs());
   const int t = ceil_div(b, V2_T);
-  const int tiles = t * (t + 1) / 2 + t * t;
-  int splits = min(max(1, ceil_div(n, 128)), max(1, (2 * 148 + tiles - 1) / tiles));
+  const int tiles = t * (t + 1);
+  int splits = min(max(1, ceil_div(n, tn_min_rows())), max(1, (2 * 148 + tiles - 1) / tiles));
   int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(t, 2 * t, splits);
   const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
                    ((uintptr_t)Y2 & 15) == 0) ? 1 : 0;
-  k_gemm_tn2<<<g, 256, tn2_smem(), s>>>(X, ldx, b, Y1, ldy, b, n, kchunk, 1, a16, P, Y2);
+  k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b, Y1, ldy, b, n, kchunk, 1, a16, P, Y2);
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b, 32), 2 * b);
-  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b, 2 * b, 1.0, b, C, ldc);
+  k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b, 2 * b, 1.0, 1, b, C, ldc);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
@@ -495,7 +525,7 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
   SCSF_TRY(dense_init_attrs());
   if (b1 <= NN2_MAX_K) {
     const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
-    k_gemm_nn2<<<ceil_div(n, V2_T), 256, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
+    k_gemm_nn2<<<ceil_div(n, V2_T), V2_NT, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
                                                             a16);
   } else {
     int b1r = (max(b1, 1) + 3) & ~3;

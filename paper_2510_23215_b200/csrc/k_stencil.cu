@@ -486,6 +486,15 @@ __device__ __forceinline__ double lds1a(unsigned a) {
 __device__ __forceinline__ void sts2a(unsigned a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// distributed shared memory: 32-bit shared::cluster addresses (mapa) and stores
+__device__ __forceinline__ unsigned mapa32(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void stc2a(unsigned a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
 
 template <int CS, int CB>
 __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
@@ -579,10 +588,14 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     acur[cc] = sbase + 8u * (unsigned)((2 * cc) * pitch + l0);
     anxt[cc] = sbase + 8u * (unsigned)((2 * cc + 1) * pitch + l0);
   }
+  // shared::cluster addresses: the lower row of my patch in the CTA below's top ghost row,
+  // and my row(s) in the CTA above's bottom ghost row, as deltas to my own target address
+  const unsigned lo32 = has_lo ? mapa32(sbase, rank - 1) : 0u, hi32 = has_hi ? mapa32(sbase, rank + 1) : 0u;
+  const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
+  const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
   for (int st = 0; st < m; ++st) {
     const double a = sa[st], bco = sb[st];
-    const int nofs = ((st + 1) & 1) ? pitch : 0;            // target buffer of the DSMEM pushes
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) {
       if (cc < ncb) {                                      // uniform across the CTA
@@ -612,10 +625,10 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
         if (act) sts2a(na, v);
         if (up_ok) sts2a(na + nx8, u);
-        const int colofs = 2 * cc * pitch + nofs;
-        if (push_lo0) sts2(lo_buf + colofs + (R + 1) * nx + xq, v);
-        if (push_hi0) sts2(hi_buf + colofs + xq, v);
-        if (push_hi1) sts2(hi_buf + colofs + xq, u);
+        // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas)
+        if (push_lo0) stc2a(na + dlo, v);
+        if (push_hi0) stc2a(na + dhi, v);
+        if (push_hi1) stc2a(na + dhi, u);
         acur[cc] = na;
         anxt[cc] = ca;
       }

@@ -43,6 +43,7 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
 int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y2, int64_t ldy, int b, int64_t n,
                  double* C, int64_t ldc, double* P, cudaStream_t s);
+int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s);
 size_t small_scratch_doubles(int b);
 int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Rinv, double* scratch,
                   Ctrl* ctrl, cudaStream_t s);
@@ -202,7 +203,8 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(gemm_tn_dual(Va, w.ldv, Va, Wa, w.ldv, ba, w.n, w.C2, ba, w.P, s));
   if (w.comm) SCSF_TRY(w.comm->allreduce_sum(w.C2, (size_t)2 * bb, s));
   const double* S2 = w.C2;
-  const double* H = w.C2 + bb;
+  double* H = w.C2 + bb;
+  SCSF_TRY(symm_upper_impl(H, ba, ba, s));                                                 // H = Q1^T A Q1 (symmetric)
   SCSF_TRY(chol_inv_impl(S2, ba, ba, w.n_glob, w.Rinv, w.Gwork, w.ctrl, s));
   SCSF_TRY(gemm_nn_ex(H, ba, ba, ba, w.Rinv, ba, ba, 1.0, 0.0, w.Tb, ba, 1, s));         // T = H R2^{-1}
   SCSF_TRY(gemm_tn(w.Rinv, ba, ba, w.Tb, ba, ba, ba, 1.0, 1, w.S, ba, w.P, s));           // G = R2^{-T} T (upper)
