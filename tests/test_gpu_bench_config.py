@@ -1,0 +1,85 @@
+"""Parity at BASELINE.json's full size in the launch configuration bench.py times — GPU.
+
+configs[1] (C2): N = 1000 operators, sorted queue cut into 32 concurrent chains
+(`scsf_solve_chains`), exactly as bench.py runs it.  Every operator's pairs are
+checked by properties that hold at any size (residual, orthonormality, sorted,
+Loewner bounds); a sample (chain heads, chain tails, seeded picks) is compared
+with the oracle's own eigenpairs (oracle/eig.py, shift-invert block Lanczos).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import checks
+from tests.helpers import check_pairs, device_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_23215_b200 import scsf
+    scsf.load_library()
+    return scsf
+
+
+def _stencil_apply(coef, nx, ny, V):
+    """A V for a symmetric 5-point DIA operator (test-side torch; coef [3, ld], V [k, ld])."""
+    import torch
+    n = nx * ny
+    d, cx, cy = coef[0, :n], coef[1, :n], coef[2, :n]
+    X = V[:, :n]
+    Y = d * X
+    Y[:, :-1] += cx[:-1] * X[:, 1:]
+    Y[:, 1:] += cx[:-1] * X[:, :-1]
+    Y[:, :-nx] += cy[:-nx] * X[:, nx:]
+    Y[:, nx:] += cy[:-nx] * X[:, :-nx]
+    return Y
+
+
+def test_c2_full_queue_32_chains(lib):
+    import torch
+    cfg = synth.get_config("C2")
+    f = synth.make_batch(cfg)
+    assert f.n_ops == 1000
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    n_chains = 32
+    evals, evecs, stats = lib.solve_chains(ops, perm, n_chains, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter,
+                                           seed=12345)
+    torch.cuda.synchronize()
+    assert all(s["status"] == 0 for s in stats), [i for i, s in enumerate(stats) if s["status"] != 0]
+    n = cfg.n
+    worst_r = worst_o = 0.0
+    for k in range(len(perm)):
+        op = int(perm[k])
+        V = evecs[k, :, :].contiguous()                      # [L, ld]
+        lam = evals[k]
+        assert bool(torch.all(lam[1:] >= lam[:-1]))
+        AV = _stencil_apply(ops.coef[op], cfg.nx, cfg.nx, V)
+        R = AV - lam[:, None] * V[:, :n]
+        c = ops.coef[op, :, :n].abs()
+        rows = c[0] + c[1] + c[2]
+        rows[1:] += c[1, :-1]
+        rows[cfg.nx:] += c[2, :-cfg.nx]
+        normA = float(rows.max())                          # ||A||_inf (Gershgorin row sums)
+        r = float((R.norm(dim=1) / normA).max())
+        G = V[:, :n] @ V[:, :n].T
+        o = float((G - torch.eye(cfg.L, dtype=G.dtype, device=G.device)).abs().max())
+        worst_r, worst_o = max(worst_r, r), max(worst_o, o)
+    assert worst_r <= 1e-8, worst_r          # north star: ||Ax - lx|| / ||A|| <= 1e-8 for every pair
+    assert worst_o <= 1e-12, worst_o
+    # oracle on a sample: heads and tails of some chains, plus seeded picks
+    starts = lib.split_chains(len(perm), n_chains)
+    rng = np.random.default_rng(0)
+    sample = {0, int(starts[1]) - 1, int(starts[7]), int(starts[20]) - 1, len(perm) - 1}
+    sample |= set(int(x) for x in rng.choice(len(perm), 3, replace=False))
+    ev = evals.cpu().numpy()
+    for k in sorted(sample):
+        op = int(perm[k])
+        check_pairs(f, op, ev[k], evecs[k, :, :n].cpu().numpy().T, cfg.L, paper_tol=10 * cfg.tol)
+    lo, hi = checks.loewner_bounds(f, int(perm[0]), cfg.L)
+    assert np.all(lo <= ev[0] * (1 + 1e-12)) and np.all(ev[0] <= hi * (1 + 1e-12))
