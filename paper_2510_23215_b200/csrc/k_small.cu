@@ -824,6 +824,19 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
   }
 }
 
+// First-filter bounds of a warm solve from the previous operator's ascending Ritz values
+__global__ void k_bounds_from_theta(const double* __restrict__ theta, int b, Ctrl* ctrl, double* fp) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double lam = theta[0], alpha = theta[b - 1], beta = ctrl->beta;
+  double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
+  if (!(e > 0.0)) e = fmax(fabs(beta), 1.0) * 1e-12;
+  ctrl->lambda = lam;
+  ctrl->alpha = alpha;
+  fp[0] = lam;
+  fp[1] = c;
+  fp[2] = e;
+}
+
 __global__ void k_ctrl_init(Ctrl* ctrl, const unsigned long long* gersh) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   ctrl->beta = __longlong_as_double((long long)*gersh);
@@ -1141,6 +1154,12 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
               double tol, Ctrl* ctrl, double* fp, cudaStream_t s) {
   k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s) {
+  k_bounds_from_theta<<<1, 32, 0, s>>>(theta_sorted, b, ctrl, fp);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

@@ -52,6 +52,7 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
               double tol, Ctrl* ctrl, double* fp, cudaStream_t s);
 int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
+int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s);
 int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s);
 int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncols, double* send_lo,
                    double* send_hi, cudaStream_t s);
@@ -220,6 +221,16 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   }
   SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
   return SCSF_OK;
+}
+
+// R11 (default) or the paper-literal inherited bounds (SCSF_INHERIT_BOUNDS=1), see DESIGN.md
+static bool inherit_bounds() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_INHERIT_BOUNDS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 // ---- optional phase timers (scsf_set_timing) ----
@@ -406,9 +417,15 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
   }
-  // one Rayleigh-Ritz of the new operator on the initial block (R11)
-  SCSF_TRY(rayleigh_ritz(ops, op, w, 0, L, tol, spmm_cols, s));
-  SCSF_TRY(read_ctrl(w, h, s));
+  if (warm && !orthonormalize && inherit_bounds()) {
+    // P:193-194, P:297 read literally: the first filter of a warm solve uses the previous
+    // operator's Ritz values (lambda = theta_1, alpha = theta_b) and this operator's beta
+    SCSF_TRY(bounds_from_theta_impl(w.theta_sorted, b, w.ctrl, w.fp, s));
+  } else {
+    // one Rayleigh-Ritz of the new operator on the initial block (R11)
+    SCSF_TRY(rayleigh_ritz(ops, op, w, 0, L, tol, spmm_cols, s));
+    SCSF_TRY(read_ctrl(w, h, s));
+  }
   int kL = h.kL;
   int fallbacks = 0;
   // One outer iteration (steps 1-6) as device work only; replayed from a CUDA graph
