@@ -223,12 +223,14 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   return SCSF_OK;
 }
 
-// R11 (default) or the paper-literal inherited bounds (SCSF_INHERIT_BOUNDS=1), see DESIGN.md
+// Warm solves start filtering with the previous operator's Ritz values (the paper's
+// P:193-194 / P:297, reading R11); SCSF_INHERIT_BOUNDS=0 restores the extra Rayleigh-Ritz of
+// the new operator before the first filter.
 static bool inherit_bounds() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SCSF_INHERIT_BOUNDS");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
