@@ -74,7 +74,7 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
 bool filter_resident_ok(const scsf_ops* ops);
 int filter_kind(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
-                         const double* fp, int m, cudaStream_t s);
+                         const double* fp, int m, cudaStream_t s, const int* deg = nullptr);
 
 }  // namespace scsf
 

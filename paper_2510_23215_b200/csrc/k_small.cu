@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restric
 // theta/res/wn/rel are indexed by block column (0..b-1); active columns [kL, b).
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
                        const double* __restrict__ wn, double* __restrict__ rel, int b, int L,
-                       double tol, Ctrl* ctrl, double* fp) {
+                       double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg) {
   const int lane = threadIdx.x;            // one warp
   const int kL = ctrl->kL;
   int first_bad = b, nonfin = 0;
@@ -821,6 +821,44 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
       fp[1] = c;
       fp[2] = e;
     }
+  }
+  // SURVEY f2 (Alg. 1 l. 5's staggered update, ChASE-style): per-column degree for the next
+  // filter.  A column with relative residual r and scaled Ritz value t = (theta - c)/e gains a
+  // factor g = |t| + sqrt(t^2 - 1) per degree over the damped interval, so reaching
+  // 0.1 tol takes ceil(ln(10 r / tol) / ln g) steps; clamped to [4, m] and made non-decreasing
+  // in the column index (Ritz order).  deg == NULL: uniform degree m (reading R8).
+  if (deg) {
+    __syncwarp();
+    const int kLn = ctrl->kL;
+    const double c = fp[1], e = fp[2];
+    int run = 4, sum = 0;
+    for (int base = kLn; base < b; base += 32) {
+      const int j = base + lane;
+      int mj = mdeg;
+      if (j < b) {
+        const double t = fabs((theta[j] - c) / e), r = rel[j];
+        if (t > 1.0 && isfinite(r)) {
+          const double g = t + sqrt((t - 1.0) * (t + 1.0));
+          const double need = log(fmax(10.0 * r / tol, 1.0)) / log(g);
+          mj = (int)fmin((double)mdeg, fmax(4.0, ceil(need)));
+        }
+      }
+      // running maximum across the columns (lane order, then chunk order)
+      int v = mj;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = max(v, u);
+      }
+      v = max(v, run);
+      if (j < b) {
+        deg[j] = v;
+        sum += v;
+      }
+      run = __shfl_sync(0xffffffffu, v, 31);
+    }
+    sum = (int)warp_sum((double)sum);
+    if (lane == 0) ctrl->pad[1] = sum;
   }
 }
 
@@ -1152,8 +1190,18 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 }
 
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
-              double tol, Ctrl* ctrl, double* fp, cudaStream_t s) {
-  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp);
+              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, cudaStream_t s) {
+  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp, deg, mdeg);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
+__global__ void k_fill_int(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+int fill_int_impl(int* p, int n, int v, cudaStream_t s) {
+  k_fill_int<<<ceil_div(n, 256), 256, 0, s>>>(p, n, v);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

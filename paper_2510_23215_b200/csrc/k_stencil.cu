@@ -499,7 +499,8 @@ __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
 template <int CS, int CB>
 __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
-                                                       double* __restrict__ Out, const double* __restrict__ fp, int m) {
+                                                       double* __restrict__ Out, const double* __restrict__ fp, int m,
+                                                       const int* __restrict__ deg) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
   __shared__ double sa[128], sb[128];                      // per-step scalars (m <= 128)
@@ -514,6 +515,14 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const int pitch = (R + 2) * nx;                          // one buffer of one column
   const int n = nx * ny;
   const int ncb = min(CB, ncols - j0);                     // columns of this CTA (uniform)
+  // per-column degree (deg == NULL: uniform m), uniform across the cluster
+  int mcol[CB];
+  int mrun = 0;
+#pragma unroll
+  for (int cc = 0; cc < CB; ++cc) {
+    mcol[cc] = (cc < ncb) ? (deg ? max(1, min(m, deg[j0 + cc])) : m) : 0;
+    mrun = max(mrun, mcol[cc]);
+  }
   const double c = fp[1];
   if (tid == 0) {                                          // Alg. 1 scalars, same operation sequence as step_scalars()
     const double lam = fp[0], e = fp[2];
@@ -594,11 +603,11 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
   const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
-  for (int st = 0; st < m; ++st) {
+  for (int st = 0; st < mrun; ++st) {
     const double a = sa[st], bco = sb[st];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) {
-      if (cc < ncb) {                                      // uniform across the CTA
+      if (st < mcol[cc]) {                                 // uniform across the CTA (0 beyond ncb)
         const unsigned ca = acur[cc], na = anxt[cc];
         const double2 xd = lds2a(ca - nx8);
         const double2 xa = lds2a(ca);
@@ -636,7 +645,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
   }
   for (int cc = 0; cc < ncb; ++cc) {
-    const double* fin = cbuf + (size_t)(2 * cc + (m & 1)) * pitch;
+    const double* fin = cbuf + (size_t)(2 * cc + (mcol[cc] & 1)) * pitch;
     double* out = Out + (int64_t)(j0 + cc) * ldv;
     for (int q = tid; q < rows * hx; q += nthr)
       *reinterpret_cast<double2*>(out + row0 * nx + 2 * q) = lds2(fin + nx + 2 * q);
@@ -824,23 +833,25 @@ bool filter_resident_ok(const scsf_ops* ops) {
 
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
-                              int64_t ldv, int ncols, double* Out, const double* fp, int m) {
-  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
+                              int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
+  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 template <int CS>
 static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* cf, int64_t ldc, int nx, int ny,
-                                const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m) {
-  if (cb == 4) return launch_cl1<CS, 4>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
-  if (cb == 2) return launch_cl1<CS, 2>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
-  return launch_cl1<CS, 1>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
+                                const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m,
+                                const int* deg) {
+  if (cb == 4) return launch_cl1<CS, 4>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  if (cb == 2) return launch_cl1<CS, 2>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  return launch_cl1<CS, 1>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 static cudaError_t launch_cl(cudaLaunchConfig_t& cfg, int cs, int cb, const double* cf, int64_t ldc, int nx, int ny,
-                             const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m) {
+                             const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m,
+                             const int* deg) {
   switch (cs) {
-    case 1: return launch_cl_cb<1>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
-    case 2: return launch_cl_cb<2>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
-    case 4: return launch_cl_cb<4>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
-    default: return launch_cl_cb<8>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m);
+    case 1: return launch_cl_cb<1>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    case 2: return launch_cl_cb<2>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    case 4: return launch_cl_cb<4>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    default: return launch_cl_cb<8>(cfg, cb, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   }
 }
 
@@ -867,7 +878,7 @@ int stencil_init_attrs() {
 
 // Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
-                         const double* fp, int m, cudaStream_t s) {
+                         const double* fp, int m, cudaStream_t s, const int* deg) {
   if (ncols <= 0) return SCSF_OK;
   const int n = ops->nx * ops->ny;
   const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
@@ -894,7 +905,7 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SCSF_CUDA_CHECK(launch_cl(cfg, cs, cb, cf, ops->ld, ops->nx, ops->ny, X, ldv, ncols, Out, fp, m));
+    SCSF_CUDA_CHECK(launch_cl(cfg, cs, cb, cf, ops->ld, ops->nx, ops->ny, X, ldv, ncols, Out, fp, m, deg));
   } else if (quad && n <= 4 * RQ_T * RQ_Q)
     k_filter_res2d_q<<<ncols, RQ_T, (size_t)2 * n * sizeof(double), s>>>(cf, ops->ld, ops->nx, n, X, ldv, Out, fp, m);
   else

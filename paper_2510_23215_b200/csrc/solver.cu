@@ -30,7 +30,7 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
                  int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s);
 bool filter_resident_ok(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
-                         const double* fp, int m, cudaStream_t s);
+                         const double* fp, int m, cudaStream_t s, const int* deg = nullptr);
 int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
                const double* theta, double* res, double* wn, cudaStream_t s);
 int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s);
@@ -50,7 +50,7 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
 int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
                 double* Zout, Ctrl* ctrl, cudaStream_t s);
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
-              double tol, Ctrl* ctrl, double* fp, cudaStream_t s);
+              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, cudaStream_t s);
 int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
 int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s);
 int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s);
@@ -109,6 +109,7 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.ctrl = a.take<Ctrl>(1);
   w.gersh = a.take<unsigned long long>(1);
   w.coef_buf = a.take<double>((int64_t)(1 + ops->dim) * ops->ld);
+  w.deg = a.take<int>(b);
   if (dist && dist->comm) {
     const int64_t hb = (int64_t)b * ops->nx;
     w.send_lo = a.take<double>(hb);
@@ -183,7 +184,7 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
     SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
   }
-  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, s));
   return SCSF_OK;
 }
 
@@ -219,7 +220,7 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
     SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
   }
-  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, s));
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, s));
   return SCSF_OK;
 }
 
@@ -234,6 +235,17 @@ static bool inherit_bounds() {
   }
   return v == 1;
 }
+
+// per-column filter degree (SCSF_ADAPTIVE_DEGREE=1; default: uniform degree, R8)
+static bool adaptive_degree() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_ADAPTIVE_DEGREE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+int fill_int_impl(int* p, int n, int v, cudaStream_t s);
 
 // ---- optional phase timers (scsf_set_timing) ----
 static int g_timing = 0;
@@ -414,6 +426,9 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   Ctrl h{};
   SCSF_TRY(gershgorin_impl(ops, op, w.gersh, s));
   SCSF_TRY(ctrl_init_impl(w.ctrl, w.gersh, s));
+  w.mdeg = degree;
+  w.deg_on = (adaptive_degree() && !w.comm && filter_resident_ok(ops)) ? w.deg : nullptr;
+  if (w.deg_on) SCSF_TRY(fill_int_impl(w.deg, b, degree, s));
   if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, w.goff, s));
   if (!warm || orthonormalize) {
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
@@ -430,6 +445,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   }
   int kL = h.kL;
   int fallbacks = 0;
+  int64_t next_colsteps = (int64_t)degree * (b - kL);      // per-column degrees start at m
   // One outer iteration (steps 1-6) as device work only; replayed from a CUDA graph
   // keyed by kL (every pointer and shape of the iteration is a function of kL).
   auto iteration = [&](int kLc) -> int {
@@ -439,7 +455,8 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     SCSF_TRY(tm.mark(0, s));
     double* F;
     if (!w.comm && filter_resident_ok(ops)) {
-      SCSF_TRY(filter_resident_impl(ops, op, y[0], y[1], w.ldv, ba, w.fp, degree, s));
+      SCSF_TRY(filter_resident_impl(ops, op, y[0], y[1], w.ldv, ba, w.fp, degree, s,
+                                    w.deg_on ? w.deg_on + kLc : nullptr));
       F = y[1];
     } else {
       SCSF_TRY(spmm(ops, op, w, y[0], nullptr, y[1], ba, 0, s));
@@ -487,11 +504,14 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     }
     // algorithmic bytes: first step reads Y0 + writes Y1, later steps read Y_s, Y_{s-1}
     // and write Y_{s+1}; one pass over the coefficient arrays per step
-    filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * ba * (degree - 1) + coef_bytes * degree;
+    // column-steps of this filter: m b_act, or the sum of the per-column degrees (f2)
+    const int64_t colsteps = w.deg_on ? next_colsteps : (int64_t)degree * ba;
+    filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * (double)(colsteps - ba) + coef_bytes * degree;
     filter_steps += degree;
-    spmm_cols += (int64_t)degree * ba + 2 * ba;
+    spmm_cols += colsteps + 2 * ba;
     SCSF_TRY(read_ctrl(w, h, s));
     SCSF_TRY(tm.accumulate());
+    next_colsteps = h.pad[1];
     if (h.chol_fail) {
       // shifted CholQR was needed: one more CholQR pass, then redo the RR step
       ++fallbacks;

@@ -21,6 +21,9 @@ struct SolveWS {
   double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;  // [b][nx] halos
   double *colbuf = nullptr, *colgath = nullptr;                        // sign convention (3 b, world 3 b)
   double* coef_buf = nullptr;                                          // this operator's arrays (graph replay)
+  int* deg = nullptr;                                                  // per-column filter degree
+  int* deg_on = nullptr;                                               // == deg when the adaptive degree is on
+  int mdeg = 20;
   int b = 0;
   double *V = nullptr, *W = nullptr, *T1 = nullptr, *T2 = nullptr;   // n x b blocks (ld ldv)
   double *S = nullptr, *Rinv = nullptr, *Zs = nullptr, *Zwork = nullptr, *Gwork = nullptr;  // b x b
