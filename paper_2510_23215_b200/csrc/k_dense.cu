@@ -25,66 +25,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // ------------------------------------------------------------- gemm_tn ----
-constexpr int TN_BM = 64, TN_KC = 16, TN_LDS = TN_KC + 4;
-
-__global__ void __launch_bounds__(128) k_gemm_tn(const double* __restrict__ X, int64_t ldx, int b1,
-                                                 const double* __restrict__ Y, int64_t ldy, int b2,
-                                                 int64_t n, int64_t kchunk, double* __restrict__ P) {
-  __shared__ __align__(16) double xs[TN_BM][TN_LDS];
-  __shared__ __align__(16) double ys[TN_BM][TN_LDS];
-  const int i0 = blockIdx.x * TN_BM, j0 = blockIdx.y * TN_BM;
-  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t kend = min(n, kbeg + kchunk);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  const int lc = threadIdx.x >> 1;          // column this thread loads (0..63)
-  const int lk = (threadIdx.x & 1) * 8;     // 8 consecutive k
-  for (int64_t k0 = kbeg; k0 < kend; k0 += TN_KC) {
-    {
-      const int ci = i0 + lc, cj = j0 + lc;
-      const bool full = (k0 + TN_KC <= kend);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        int64_t k = k0 + lk + q;
-        bool ok = full || k < kend;
-        xs[lc][lk + q] = (ok && ci < b1) ? X[k + (int64_t)ci * ldx] : 0.0;
-        ys[lc][lk + q] = (ok && cj < b2) ? Y[k + (int64_t)cj * ldy] : 0.0;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < TN_KC; kk += 4) {
-      double a[4], b[4];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = xs[wm + mi * 8 + g][kk + t];
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = ys[wn + ni * 8 + g][kk + t];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-    }
-    __syncthreads();
-  }
-  double* out = P + (int64_t)blockIdx.z * b1 * b2;
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int i = i0 + wm + mi * 8 + g;
-        int j = j0 + wn + ni * 8 + 2 * t + e;
-        if (i < b1 && j < b2) out[i + (int64_t)j * b1] = acc[mi][ni][e];
-      }
-}
+constexpr int TN_BM = 64;
 
 // C[i + j ldc] = alpha * sum_z P[z][i + j b1].  Warp w sums z = w, w+8, ... (ascending);
 // the 8 warp sums are then added in warp order: a fixed order, so deterministic.

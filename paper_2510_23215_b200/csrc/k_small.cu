@@ -331,202 +331,6 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Gin,
     for (int x = tx; x < b; x += 32) Zout[x + (int64_t)rank_s[i] * b] = Z[x + i * b];
 }
 
-// ------------------------------------------------------ jacobi_eig (xor) ----
-// Same two-sided cyclic Jacobi, for b <= 128, with the "hypercube" parallel
-// ordering: round m = 1..B-1 (B = b rounded up to a power of two) rotates the
-// B/2 disjoint pairs (p, p ^ m); every pair occurs exactly once per sweep.
-// Z lives in registers: thread (warp w, lane l) owns rows x = w*S + sx and
-// columns p = l + 32 sp (S = B/32), so the partner column p ^ m is at lane
-// l ^ (m & 31), slot sp ^ (m >> 5): one __shfl_xor per element, no shared
-// memory traffic for Z.  G keeps only its upper triangle in shared memory
-// (pitch B + 1).  Indices >= b are inert (zero rows/columns, never rotated).
-// Z <- Z J for one round: partner column p ^ m lives in lane ^ (m & 31), slot sp ^ SM.
-// Slots sp and sp ^ SM are processed together so both partner values are read
-// (shuffled) before either is overwritten.
-template <int S, int SM>
-__device__ __forceinline__ void zrot(double (&z)[S][S], int lane, int m, const double* cs_c, const double* cs_s,
-                                     const int* cs_rot) {
-  const int lm = m & 31;
-#pragma unroll
-  for (int sp = 0; sp < S; ++sp) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int sq = sp ^ SM;
-    if (sq < sp) continue;                          // handled with its partner slot
-    const int pa = lane + 32 * sp, pb = lane + 32 * sq;
-    const int qa = pa ^ m, qb = pb ^ m;
-    const int loa = min(pa, qa), lob = min(pb, qb);
-    const int rota = cs_rot[loa], rotb = cs_rot[lob];
-    const double ca = cs_c[loa], sa = (pa < qa) ? -cs_s[loa] : cs_s[loa];
-    const double cb = cs_c[lob], sb = (pb < qb) ? -cs_s[lob] : cs_s[lob];
-#pragma unroll
-    for (int sx = 0; sx < S; ++sx) {
-      const double za = z[sx][sp], zb = z[sx][sq];
-      const double pa_v = __shfl_xor_sync(0xffffffffu, zb, lm);   // partner of slot sp: slot sq of lane ^ lm
-      const double pb_v = __shfl_xor_sync(0xffffffffu, za, lm);   // partner of slot sq: slot sp of lane ^ lm
-      if (rota) z[sx][sp] = fma(ca, za, sa * pa_v);
-      if (sq != sp && rotb) z[sx][sq] = fma(cb, zb, sb * pb_v);
-    }
-  }
-}
-
-template <int LOGB>
-__global__ void __launch_bounds__(1024, 1) k_jacobi_x(const double* __restrict__ Gin, int64_t ldg, int b,
-                                                      double* __restrict__ theta_out, double* __restrict__ Zout,
-                                                      int max_sweeps, Ctrl* ctrl) {
-  constexpr int B = 1 << LOGB;
-  constexpr int S = B / 32;
-  constexpr int GP = B + 1;
-  constexpr int H2 = B / 2;
-  extern __shared__ double G[];                     // [B][GP], upper triangle used
-  __shared__ double cs_c[B], cs_s[B], cs_t[B];
-  __shared__ int cs_rot[B];
-  __shared__ int rank_s[B];
-  __shared__ double red[32];
-  __shared__ double floor_s;
-  __shared__ int any_rot[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double tol = 1e-14;
-
-  double dmax = 0.0;
-  for (int idx = tid; idx < B * B; idx += 1024) {
-    const int i = idx >> LOGB, j = idx & (B - 1);
-    if (i <= j) {
-      const double v = (i < b && j < b) ? Gin[i + (int64_t)j * ldg] : 0.0;
-      G[i * GP + j] = v;
-      if (i == j) dmax = fmax(dmax, fabs(v));
-    }
-  }
-  dmax = warp_max(dmax);
-  if (lane == 0) red[warp] = dmax;
-  double z[S][S];
-#pragma unroll
-  for (int sx = 0; sx < S; ++sx)
-#pragma unroll
-    for (int sp = 0; sp < S; ++sp) z[sx][sp] = ((warp * S + sx) == (lane + 32 * sp)) ? 1.0 : 0.0;
-  if (tid < 2) any_rot[tid] = 0;
-  __syncthreads();
-  if (tid == 0) {
-    double v = 0.0;
-    for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
-    floor_s = 4.0 * 2.220446049250313e-16 * v;
-  }
-  __syncthreads();
-  const double gfloor = floor_s;
-
-  int sweep = 0;
-  for (; sweep <= max_sweeps; ++sweep) {
-    double mx = 0.0;
-    for (int i = warp; i < b; i += 32)
-      for (int j = i + 1 + lane; j < b; j += 32) {
-        const double g = fabs(G[i * GP + j]);
-        if (g > gfloor) mx = fmax(mx, g / fmax(sqrt(fabs(G[i * GP + i] * G[j * GP + j])), 1e-300));
-      }
-    mx = warp_max(mx);
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    if (tid == 0) {
-      double v = 0.0;
-      for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
-      red[0] = v;
-    }
-    __syncthreads();
-    const bool done = red[0] <= tol;
-    __syncthreads();
-    if (done || sweep == max_sweeps) break;
-    for (int m = 1; m < B; ++m) {
-      const int h = 31 - __clz(m);                  // pairs: lo has bit h clear, hi = lo ^ m
-      const int par = m & 1;
-      if (tid < B && !((tid >> h) & 1)) {
-        const int lo = tid, hi = tid ^ m;
-        double c = 1.0, sn = 0.0, t = 0.0;
-        int rot = 0;
-        if (hi < b) {
-          const double gpq = G[lo * GP + hi], gpp = G[lo * GP + lo], gqq = G[hi * GP + hi];
-          if (fabs(gpq) > tol * sqrt(fabs(gpp * gqq)) && fabs(gpq) > gfloor) {
-            const double th = (gqq - gpp) / (2.0 * gpq);
-            t = (fabs(th) > 1e150) ? 0.5 / th : copysign(1.0, th) / (fabs(th) + sqrt(1.0 + th * th));
-            c = rsqrt(1.0 + t * t);
-            sn = t * c;
-            rot = 1;
-            any_rot[par] = 1;
-          }
-        }
-        cs_c[lo] = c; cs_s[lo] = sn; cs_t[lo] = t; cs_rot[lo] = rot;
-      }
-      if (tid == 0) any_rot[par ^ 1] = 0;           // reset the flag of the next round
-      __syncthreads();
-      if (!any_rot[par]) continue;                  // uniform: nothing to apply this round
-      // ---- G <- J^T G J on blocks {ilo, ihi} x {jlo, jhi}, ilo <= jlo (upper storage)
-      const int lowmask = (1 << h) - 1;
-#pragma unroll
-      for (int ai = warp; ai < H2; ai += 32) {
-        const int ilo = ((ai & ~lowmask) << 1) | (ai & lowmask);      // insert a 0 bit at position h
-        const int ihi = ilo ^ m;
-        const int r1 = cs_rot[ilo];
-        const double c1 = cs_c[ilo], s1 = cs_s[ilo];
-#pragma unroll
-        for (int aj = lane; aj < H2; aj += 32) {
-          if (aj < ai) continue;
-          const int jlo = ((aj & ~lowmask) << 1) | (aj & lowmask);
-          const int r2 = cs_rot[jlo];
-          if (!r1 && !r2) continue;
-          const int jhi = jlo ^ m;
-          if (ilo == jlo) {
-            const int ipq = ilo * GP + ihi;
-            const double gpq = G[ipq], t = cs_t[ilo];
-            G[ilo * GP + ilo] -= t * gpq;
-            G[ihi * GP + ihi] += t * gpq;
-            G[ipq] = 0.0;
-            continue;
-          }
-          const double c2 = cs_c[jlo], s2 = cs_s[jlo];
-          const int ia = ilo * GP + jlo;                                // ilo < jlo
-          const int ib = ilo * GP + jhi;                                // ilo < jhi
-          const int ic = min(ihi, jlo) * GP + max(ihi, jlo);
-          const int id = min(ihi, jhi) * GP + max(ihi, jhi);
-          const double a = G[ia], bb = G[ib], cc = G[ic], d = G[id];
-          const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;    // columns jlo, jhi
-          const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
-          G[ia] = c1 * a2 - s1 * c2v;                                   // rows ilo, ihi
-          G[ib] = c1 * b2 - s1 * d2;
-          G[ic] = s1 * a2 + c1 * c2v;
-          G[id] = s1 * b2 + c1 * d2;
-        }
-      }
-      // ---- Z <- Z J in registers (m >> 5 is uniform: dispatch to a static slot permutation)
-      const int sm = m >> 5;
-      if (S == 1 || sm == 0) zrot<S, 0>(z, lane, m, cs_c, cs_s, cs_rot);
-      else if (sm == 1) zrot<S, (S > 1 ? 1 : 0)>(z, lane, m, cs_c, cs_s, cs_rot);
-      else if (sm == 2) zrot<S, (S > 2 ? 2 : 0)>(z, lane, m, cs_c, cs_s, cs_rot);
-      else zrot<S, (S > 3 ? 3 : 0)>(z, lane, m, cs_c, cs_s, cs_rot);
-      __syncthreads();
-    }
-  }
-  if (tid == 0 && ctrl) {
-    if (sweep >= max_sweeps) ctrl->nonfinite |= 2;
-    ctrl->pad[0] += sweep;
-  }
-  if (tid < b) {
-    const double v = G[tid * GP + tid];
-    int rk = 0;
-    for (int j = 0; j < b; ++j) {
-      const double w = G[j * GP + j];
-      rk += (w < v) || (w == v && j < tid);
-    }
-    rank_s[tid] = rk;
-    theta_out[rk] = v;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int sx = 0; sx < S; ++sx)
-#pragma unroll
-    for (int sp = 0; sp < S; ++sp) {
-      const int x = warp * S + sx, pc = lane + 32 * sp;
-      if (x < b && pc < b) Zout[x + (int64_t)rank_s[pc] * b] = z[sx][sp];
-    }
-}
-
 // ------------------------------------------------ jacobi_eig (G | Z split) ----
 // The same two-sided cyclic Jacobi with the XOR ("hypercube") ordering, split
 // in two kernels so the rotation accumulator no longer competes with G for the
@@ -1044,8 +848,6 @@ int set_small_attrs() {
   if (g_small_attr) return SCSF_OK;
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)jac_smem(JAC_SMEM_MAX_B)));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_x<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       128 * 129 * (int)sizeof(double)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_g<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        128 * 129 * (int)sizeof(double)));
   g_small_attr = 1;

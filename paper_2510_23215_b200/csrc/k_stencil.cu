@@ -343,17 +343,6 @@ __global__ void __launch_bounds__(RES_T, 1) k_filter_res2d(const double* __restr
   for (int k = tid; k < (int)ldv; k += RES_T) out[k] = (k < n) ? fin[k] : 0.0;
 }
 
-// Quad variant (nx % 4 == 0): a thread owns quads of 4 consecutive x-points,
-// so the column streams move as 128-bit shared-memory accesses and the
-// coefficients as 256-bit loads (one LDG per coefficient quad): ~2.5x fewer
-// instructions per point than the scalar kernel above.  Y_{s-1} is read from
-// the target buffer (it holds the step-before-last at the same points), so no
-// per-thread register state survives a step.  x-neighbours k0-1 and
-// k0+4 are single 8-byte shared loads (their couplings cx are 0 across a row
-// end, so no row test is needed); y-neighbours are whole quads (nx % 4 == 0).
-constexpr int RQ_T = 1024;
-constexpr int RQ_Q = 3;                          // quads per thread: n <= 4 * 1024 * 3 = 12288
-
 __device__ __forceinline__ double4 lds4(const double* p) {
   const double2 a = *reinterpret_cast<const double2*>(p);
   const double2 b = *reinterpret_cast<const double2*>(p + 2);
@@ -362,84 +351,6 @@ __device__ __forceinline__ double4 lds4(const double* p) {
 __device__ __forceinline__ void sts4(double* p, double4 v) {
   *reinterpret_cast<double2*>(p) = make_double2(v.x, v.y);
   *reinterpret_cast<double2*>(p + 2) = make_double2(v.z, v.w);
-}
-
-__global__ void __launch_bounds__(RQ_T, 1) k_filter_res2d_q(const double* __restrict__ cf, int64_t ldc, int nx,
-                                                            int n, const double* __restrict__ X, int64_t ldv,
-                                                            double* __restrict__ Out, const double* __restrict__ fp,
-                                                            int m) {
-  extern __shared__ __align__(16) double rbuf[];  // [2][n]
-  const int j = blockIdx.x, tid = threadIdx.x;
-  const int nq = n >> 2;
-  const double* x0 = X + (int64_t)j * ldv;
-  double* out = Out + (int64_t)j * ldv;
-  const double lam = fp[0], c = fp[1], e = fp[2];
-  const double s1 = e / (lam - c);
-  const double* cdg = cf;
-  const double* ccx = cf + ldc;
-  const double* ccy = cf + 2 * ldc;
-#pragma unroll
-  for (int i = 0; i < RQ_Q; ++i) {
-    const int q = tid + RQ_T * i;
-    if (q < nq) sts4(rbuf + 4 * q, ldg4_nc(x0 + 4 * q));
-  }
-  __syncthreads();
-  double sig = s1;
-  for (int st = 0; st < m; ++st) {
-    double a, bco;
-    if (st == 0) {
-      a = s1 / e;
-      bco = 0.0;
-    } else {                                     // same operation sequence as step_scalars()
-      const double sn = 1.0 / (2.0 / s1 - sig);
-      a = 2.0 * sn / e;
-      bco = -sn * sig;
-      sig = sn;
-    }
-    const double* cur = rbuf + (st & 1) * n;
-    double* nxt = rbuf + ((st + 1) & 1) * n;
-#pragma unroll
-    for (int i = 0; i < RQ_Q; ++i) {
-      const int q = tid + RQ_T * i;
-      if (q >= nq) break;
-      const int k0 = 4 * q;
-      const double4 xc = lds4(cur + k0);
-      const double xl = (k0 >= 1) ? cur[k0 - 1] : 0.0;
-      const double xr = (k0 + 4 < n) ? cur[k0 + 4] : 0.0;
-      const bool hu = k0 + nx < n, hd = k0 >= nx;
-      const double4 xu = hu ? lds4(cur + k0 + nx) : make_double4(0, 0, 0, 0);
-      const double4 xd = hd ? lds4(cur + k0 - nx) : make_double4(0, 0, 0, 0);
-      const double4 dg = ldg4_nc(cdg + k0);
-      const double4 cxp = ldg4_nc(ccx + k0);
-      const double cxm = (k0 >= 1) ? __ldg(ccx + k0 - 1) : 0.0;
-      const double4 cyp = ldg4_nc(ccy + k0);
-      const double4 cym = hd ? ldg4_nc(ccy + k0 - nx) : make_double4(0, 0, 0, 0);
-      double4 v;
-      v.x = fma(dg.x - c, xc.x, fma(cxp.x, xc.y, fma(cxm, xl, fma(cyp.x, xu.x, cym.x * xd.x))));
-      v.y = fma(dg.y - c, xc.y, fma(cxp.y, xc.z, fma(cxp.x, xc.x, fma(cyp.y, xu.y, cym.y * xd.y))));
-      v.z = fma(dg.z - c, xc.z, fma(cxp.z, xc.w, fma(cxp.y, xc.y, fma(cyp.z, xu.z, cym.z * xd.z))));
-      v.w = fma(dg.w - c, xc.w, fma(cxp.w, xr, fma(cxp.z, xc.z, fma(cyp.w, xu.w, cym.w * xd.w))));
-      // Y_{s-1} sits in the target buffer at the same points (written two steps ago)
-      if (st > 0) {
-        const double4 p = lds4(nxt + k0);
-        v.x = fma(bco, p.x, a * v.x);
-        v.y = fma(bco, p.y, a * v.y);
-        v.z = fma(bco, p.z, a * v.z);
-        v.w = fma(bco, p.w, a * v.w);
-      } else {
-        v.x *= a; v.y *= a; v.z *= a; v.w *= a;
-      }
-      sts4(nxt + k0, v);
-    }
-    __syncthreads();
-  }
-  const double* fin = rbuf + (m & 1) * n;
-  for (int q = tid; 4 * q < (int)ldv; q += RQ_T) {
-    const int k0 = 4 * q;
-    double4 v = make_double4(0, 0, 0, 0);
-    if (k0 < n) v = lds4(fin + k0);
-    stg4(out + k0, v);
-  }
 }
 
 // --------------------------------------- cluster-resident filter (2-D) ----
@@ -862,8 +773,6 @@ int stencil_init_attrs() {
   if (done) return SCSF_OK;
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * RES_MAX_N * (int)sizeof(double)));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       2 * 4 * RQ_T * RQ_Q * (int)sizeof(double)));
 #define SCSF_CL_ATTR(CS, CB) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
   SCSF_CL_ATTR(1, 1); SCSF_CL_ATTR(1, 2); SCSF_CL_ATTR(1, 4);
@@ -883,8 +792,6 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
   const int n = ops->nx * ops->ny;
   const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
   SCSF_TRY(stencil_init_attrs());
-  const bool quad = (ops->nx % 4 == 0) && (ldv % 4 == 0) && (ops->ld % 4 == 0) && ((uintptr_t)X % 32 == 0) &&
-                    ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0);
   const bool pair = (ops->nx % 2 == 0) && (ldv % 2 == 0) && (ops->ld % 2 == 0) && ((uintptr_t)X % 16 == 0) &&
                     ((uintptr_t)Out % 16 == 0) && ((uintptr_t)cf % 16 == 0);
   const int cs = pair ? cluster_size_for(ops) : 0;
@@ -906,9 +813,7 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     SCSF_CUDA_CHECK(launch_cl(cfg, cs, cb, cf, ops->ld, ops->nx, ops->ny, X, ldv, ncols, Out, fp, m, deg));
-  } else if (quad && n <= 4 * RQ_T * RQ_Q)
-    k_filter_res2d_q<<<ncols, RQ_T, (size_t)2 * n * sizeof(double), s>>>(cf, ops->ld, ops->nx, n, X, ldv, Out, fp, m);
-  else
+  } else
     k_filter_res2d<<<ncols, RES_T, (size_t)2 * n * sizeof(double), s>>>(cf, ops->ld, ops->nx, n, X, ldv, Out, fp, m);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
