@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
 // 64-row panel of X stays resident (so Out may alias X); M streams through a
 // 2-stage ring in k-chunks.  tri_upper: M is upper triangular, chunks with
 // k > last column of the pass are skipped.
-constexpr int NN2_MAX_K = 128;
+constexpr int NN2_MAX_K = 256;                     // panel 256 x 68 doubles (139 KB) + M ring (37 KB)
 
 __global__ void __launch_bounds__(V2_NT) k_gemm_nn2(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
                                                   const double* __restrict__ M, int64_t ldm, int b2,
