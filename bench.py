@@ -131,6 +131,13 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def lib_ws_host(ops, cfg):
+    import ctypes
+    from paper_2510_23215_b200 import scsf
+    st = ops.c_struct()
+    return scsf.load_library().scsf_solve_chains_host_workspace_bytes(ctypes.byref(st), cfg.L, cfg.nex)
+
+
 # --------------------------------------------------------------- cpu oracle ----
 def oracle_rate(cfg, params_all, fields, sample_ops: int):
     """The oracle as it stands, on the host cores: operators/s on a bounded sample."""
@@ -346,7 +353,9 @@ def main():
         out_e = torch.empty((hi - lo, cfg.L), dtype=torch.float64).pin_memory()
         out_v = torch.empty((hi - lo, cfg.L, ops.ld), dtype=torch.float64).pin_memory() if args.e2e_vecs else None
         h2d = hp.numel() * 8 + sum(f.numel() * 8 for f in hf) + hc.numel() * 8
-        d2h = out_e.numel() * 8 + (out_v.numel() * 8 if out_v is not None else 0)
+        d2h = (hi - lo) * cfg.L * 8 + ((hi - lo) * cfg.L * cfg.n * 8 if out_v is not None else 0)
+
+        hws = scsf._workspace(lib_ws_host(ops, cfg) * n_chains, dev)
 
         def e2e_step():
             dp = hp.to(dev, non_blocking=True)
@@ -355,13 +364,9 @@ def main():
             o = scsf.assemble(cfg.dim, cfg.nx, cfg.h, dfs, dc)
             perm, _, _ = scsf.sort(dp, cfg.dim, cfg.nx, cfg.p0)
             chain = np.array([g2l[int(g)] for g in perm[lo:hi]], dtype=np.int32)
-            ev, vv, _ = scsf.solve_chains(o, chain, n_chains, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter,
-                                          seed=12345, ws=ws, evals=evals,
-                                          evecs=evecs if out_v is not None else None,
-                                          want_vecs=out_v is not None, raise_on_fail=False)
-            out_e.copy_(ev, non_blocking=True)
-            if out_v is not None:
-                out_v.copy_(vv, non_blocking=True)
+            # pairs stream to the pinned host buffers while the chains run (scsf_solve_chains_host)
+            scsf.solve_chains_host(o, chain, n_chains, cfg.L, cfg.nex, out_e, out_v, cfg.degree, cfg.tol,
+                                   cfg.max_iter, seed=12345, raise_on_fail=False, ws=hws)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -384,8 +389,9 @@ def main():
             ems = float(t.item())
         e2e = {"value": N / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": k2, "ms_per_step": ems,
-               "what": "pinned host fields -> H2D -> scsf_assemble -> scsf_sort -> scsf_solve_queue -> D2H evals"
-                       + (" + evecs" if out_v is not None else "")}
+               "what": "pinned host fields -> H2D -> scsf_assemble -> scsf_sort -> scsf_solve_chains_host (evals"
+                       + (" + evecs" if out_v is not None else "") + " streamed D2H into pinned host memory while "
+                       "the chains run)"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None

@@ -211,6 +211,23 @@ int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* 
                       int32_t max_iter, uint64_t seed, double* evals, double* evecs, int64_t ld_vec,
                       scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
 
+/*
+ * scsf_solve_chains with the results streamed to pinned host memory while the
+ * chains run ("streaming eigenpair writer"; Fig. 1 steps 5-6,
+ * P:49): after each operator its L Ritz pairs are staged on the device
+ * (double buffer per chain) and copied to the host on a second stream, so the
+ * device-to-host traffic overlaps the next operator's solve.
+ *  evals_host  host [len][L] (pinned), by queue position
+ *  evecs_host  host [len][L][ld_host] (pinned) or NULL; ld_host >= n
+ *  ws_bytes    >= n_chains * scsf_solve_chains_host_workspace_bytes(ops, L, nex)
+ * Returns when every chain's copies have landed.  Errors as scsf_solve_chains.
+ */
+size_t scsf_solve_chains_host_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
+int scsf_solve_chains_host(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                           int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol,
+                           int32_t max_iter, uint64_t seed, double* evals_host, double* evecs_host,
+                           int64_t ld_host, scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------- row-partitioned solve ---- */
 /*
  * One operator too large for one GPU's share of the work (BASELINE.json

@@ -266,10 +266,39 @@ int scsf_solve_one(const scsf_ops* ops, int32_t op_index, int32_t L, int32_t nex
 
 // One warm-start chain on one stream: chain[0] cold, every later operator warm
 // from the previous final block.  Outputs by chain position.
+// Host outputs streamed while the chain runs (SURVEY f4 "streaming eigenpair writer"): each
+// operator's L pairs are staged on the device (double buffer) and copied to pinned host memory
+// on a second stream, overlapping the next operator's solve.
+struct HostSink {
+  double* evals = nullptr;     // host [n_chain][L]
+  double* evecs = nullptr;     // host [n_chain][L][ld] or NULL
+  int64_t ld = 0;
+  double* stage[2] = {nullptr, nullptr};      // device L x ldv each
+  double* stage_ev[2] = {nullptr, nullptr};   // device L each
+};
+
 static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
                      int32_t degree, double tol, int32_t max_iter, uint64_t seed, double* evals, double* evecs,
-                     int64_t ld_vec, scsf_stats* st, SolveWS& w, cudaStream_t s) {
-  const int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+                     int64_t ld_vec, scsf_stats* st, SolveWS& w, cudaStream_t s, HostSink* sink = nullptr) {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  if (sink) {
+    SCSF_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+      SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+  }
+  auto cleanup = [&]() {
+    if (!sink) return;
+    cudaStreamSynchronize(cs);
+    cudaStreamDestroy(cs);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(ready[i]);
+      cudaEventDestroy(done[i]);
+    }
+  };
+  const int r = [&]() -> int {
   int worst = SCSF_OK;
   for (int k = 0; k < n_chain; ++k) {
     scsf_stats local{};
@@ -278,16 +307,37 @@ static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
     if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
     if (r > worst) worst = r;
     if (st) st[k] = local;
-    SCSF_CUDA_CHECK(cudaMemcpyAsync(evals + (int64_t)k * L, w.theta_sorted, L * sizeof(double),
-                                    cudaMemcpyDeviceToDevice, s));
+    if (evals)
+      SCSF_CUDA_CHECK(cudaMemcpyAsync(evals + (int64_t)k * L, w.theta_sorted, L * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
     if (evecs)
       SCSF_CUDA_CHECK(cudaMemcpy2DAsync(evecs + (int64_t)k * L * ld_vec, ld_vec * sizeof(double), w.V,
                                         w.ldv * sizeof(double), w.n * sizeof(double), L, cudaMemcpyDeviceToDevice,
                                         s));
+    if (sink) {
+      const int b = k & 1;
+      if (k >= 2) SCSF_CUDA_CHECK(cudaStreamWaitEvent(s, done[b], 0));   // staging b is free again
+      SCSF_CUDA_CHECK(cudaMemcpyAsync(sink->stage_ev[b], w.theta_sorted, L * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+      if (sink->evecs)
+        SCSF_CUDA_CHECK(cudaMemcpy2DAsync(sink->stage[b], w.ldv * sizeof(double), w.V, w.ldv * sizeof(double),
+                                          w.n * sizeof(double), L, cudaMemcpyDeviceToDevice, s));
+      SCSF_CUDA_CHECK(cudaEventRecord(ready[b], s));
+      SCSF_CUDA_CHECK(cudaStreamWaitEvent(cs, ready[b], 0));
+      SCSF_CUDA_CHECK(cudaMemcpyAsync(sink->evals + (int64_t)k * L, sink->stage_ev[b], L * sizeof(double),
+                                      cudaMemcpyDeviceToHost, cs));
+      if (sink->evecs)
+        SCSF_CUDA_CHECK(cudaMemcpy2DAsync(sink->evecs + (int64_t)k * L * sink->ld, sink->ld * sizeof(double),
+                                          sink->stage[b], w.ldv * sizeof(double), w.n * sizeof(double), L,
+                                          cudaMemcpyDeviceToHost, cs));
+      SCSF_CUDA_CHECK(cudaEventRecord(done[b], cs));
+    }
   }
-  (void)n;
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
   return worst;
+  }();
+  cleanup();
+  return r;
 }
 
 static int check_queue(const scsf_ops* ops, const int32_t* queue, int32_t len, double* evals, double* evecs,
@@ -323,19 +373,57 @@ int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   return r;
 }
 
+static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                             int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
+                             uint64_t seed, double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws,
+                             size_t ws_bytes, void* stream, double* evals_host, double* evecs_host,
+                             int64_t ld_host);
+
+static size_t sink_bytes(const scsf_ops* ops, int L) {
+  const int64_t ldv = round_up((int64_t)ops->nx * ops->ny * ops->nz, 32);
+  return (size_t)round_up(2 * ldv * L * (int64_t)sizeof(double), 256) + (size_t)round_up(2 * L * 8, 256);
+}
+
+size_t scsf_solve_chains_host_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex) {
+  if (!ops) return 0;
+  return solve_ws_bytes(ops, L, nex) + sink_bytes(ops, L);
+}
+
+int scsf_solve_chains_host(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                           int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
+                           uint64_t seed, double* evals_host, double* evecs_host, int64_t ld_host, scsf_stats* st,
+                           void* ws, size_t ws_bytes, void* stream) {
+  SCSF_ARG_CHECK(evals_host != nullptr, "evals_host is NULL");
+  SCSF_ARG_CHECK(ops == nullptr || evecs_host == nullptr || ld_host >= (int64_t)ops->nx * ops->ny * ops->nz,
+                 "ld_host must be >= n");
+  return solve_chains_impl(ops, queue, chain_start, n_chains, L, nex, degree, tol, max_iter, seed, nullptr, nullptr,
+                           0, st, ws, ws_bytes, stream, evals_host, evecs_host, ld_host);
+}
+
 int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start, int32_t n_chains,
                       int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter, uint64_t seed,
                       double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes,
                       void* stream) {
+  return solve_chains_impl(ops, queue, chain_start, n_chains, L, nex, degree, tol, max_iter, seed, evals, evecs,
+                           ld_vec, st, ws, ws_bytes, stream, nullptr, nullptr, 0);
+}
+
+static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                             int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
+                             uint64_t seed, double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws,
+                             size_t ws_bytes, void* stream, double* evals_host, double* evecs_host,
+                             int64_t ld_host) {
+  const bool to_host = evals_host != nullptr;
   SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
   SCSF_ARG_CHECK(n_chains >= 1 && chain_start != nullptr, "n_chains >= 1 and chain_start required");
   SCSF_ARG_CHECK(chain_start[0] == 0, "chain_start[0] must be 0");
   for (int c = 0; c < n_chains; ++c)
     SCSF_ARG_CHECK(chain_start[c + 1] >= chain_start[c], "chain_start must be non-decreasing");
   const int32_t len = chain_start[n_chains];
-  SCSF_TRY(check_queue(ops, queue, len, evals, evecs, ld_vec));
+  SCSF_TRY(check_queue(ops, queue, len, to_host ? evals_host : evals, evecs, ld_vec));
   if (len == 0) return SCSF_OK;
-  const size_t per = solve_ws_bytes(ops, L, nex);
+  const size_t per_solve = solve_ws_bytes(ops, L, nex);
+  const size_t per = per_solve + (to_host ? sink_bytes(ops, L) : 0);
   if (!ws || ws_bytes < per * (size_t)n_chains) {
     set_error("workspace too small: need %zu bytes (%d chains), got %zu", per * (size_t)n_chains, n_chains,
               ws_bytes);
@@ -357,11 +445,26 @@ int scsf_solve_chains(const scsf_ops* ops, const int32_t* queue, const int32_t* 
       return;
     }
     SolveWS w;
-    int r = carve_solve_ws(ops, L, nex, (char*)ws + per * (size_t)c, per, w);
+    char* base = (char*)ws + per * (size_t)c;
+    int r = carve_solve_ws(ops, L, nex, base, per_solve, w);
     const int32_t b0 = chain_start[c], cnt = chain_start[c + 1] - chain_start[c];
+    HostSink sink;
+    if (to_host) {
+      Arena a(base + per_solve, per - per_solve);
+      double* st2 = a.take<double>(2 * w.ldv * L);
+      double* se2 = a.take<double>(2 * L);
+      sink.stage[0] = st2;
+      sink.stage[1] = st2 + w.ldv * L;
+      sink.stage_ev[0] = se2;
+      sink.stage_ev[1] = se2 + L;
+      sink.evals = evals_host + (int64_t)b0 * L;
+      sink.evecs = evecs_host ? evecs_host + (int64_t)b0 * L * ld_host : nullptr;
+      sink.ld = ld_host;
+    }
     if (r == SCSF_OK && cnt > 0)
-      r = run_chain(ops, queue + b0, cnt, L, nex, degree, tol, max_iter, seed, evals + (int64_t)b0 * L,
-                    evecs ? evecs + (int64_t)b0 * L * ld_vec : nullptr, ld_vec, st ? st + b0 : nullptr, w, s);
+      r = run_chain(ops, queue + b0, cnt, L, nex, degree, tol, max_iter, seed,
+                    evals ? evals + (int64_t)b0 * L : nullptr, evecs ? evecs + (int64_t)b0 * L * ld_vec : nullptr,
+                    ld_vec, st ? st + b0 : nullptr, w, s, to_host ? &sink : nullptr);
     status[c] = r;
     if (r != SCSF_OK) msg[c] = scsf_last_error();
     cudaStreamSynchronize(s);

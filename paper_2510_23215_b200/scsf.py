@@ -29,7 +29,7 @@ EXPORTED = [
     "scsf_dev_workspace_bytes", "scsf_gemm_tn", "scsf_gemm_nn", "scsf_chol_inv", "scsf_syev_small",
     "scsf_comm_unique_id", "scsf_comm_create", "scsf_comm_create_loopback", "scsf_comm_destroy",
     "scsf_comm_rank", "scsf_slab_rows", "scsf_solve_dist_workspace_bytes", "scsf_solve_queue_dist",
-    "scsf_filter_kind",
+    "scsf_filter_kind", "scsf_solve_chains_host_workspace_bytes", "scsf_solve_chains_host",
 ]
 
 
@@ -100,6 +100,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_chol_inv": (ctypes.c_int, [P, I64, I32, I64, P, P, SZ, P]),
         "scsf_syev_small": (ctypes.c_int, [P, I64, I32, P, P, P, P, SZ, P]),
         "scsf_filter_kind": (ctypes.c_int, [OPS]),
+        "scsf_solve_chains_host_workspace_bytes": (SZ, [OPS, I32, I32]),
+        "scsf_solve_chains_host": (ctypes.c_int, [OPS, P, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P, I64,
+                                                  ST, P, SZ, P]),
         "scsf_comm_unique_id": (ctypes.c_int, [P]),
         "scsf_comm_create": (ctypes.c_int, [I32, I32, P, ctypes.POINTER(P)]),
         "scsf_comm_create_loopback": (ctypes.c_int, [I32, P]),
@@ -341,6 +344,36 @@ def solve_chains(ops: Operators, queue, n_chains: int, L: int, nex: int, degree:
     if raise_on_fail or code != SCSF_ERR_NUMERICAL:
         _check(code)
     return evals, (evecs if want_vecs else None), [stats[i].as_dict() for i in range(nq)]
+
+
+def solve_chains_host(ops: Operators, queue, n_chains: int, L: int, nex: int, evals_host: torch.Tensor,
+                      evecs_host: torch.Tensor | None, degree: int = 20, tol: float = 1e-8, max_iter: int = 200,
+                      seed: int = 0, raise_on_fail=True, ws: torch.Tensor | None = None):
+    """Concurrent chains with the pairs streamed into pinned host tensors while the chains run
+    (scsf_solve_chains_host).  evals_host [len, L], evecs_host [len, L, ld_host] (both pinned CPU
+    float64) or None.  Returns the stats list (by queue position)."""
+    lib = load_library()
+    queue = np.ascontiguousarray(np.asarray(queue, dtype=np.int32))
+    nq = int(queue.shape[0])
+    starts = split_chains(nq, n_chains)
+    nc = len(starts) - 1
+    for t, nm in ((evals_host, "evals_host"), (evecs_host, "evecs_host")):
+        if t is not None and not (t.is_pinned() and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError(f"{nm} must be a pinned contiguous float64 CPU tensor")
+    st = ops.c_struct()
+    per = lib.scsf_solve_chains_host_workspace_bytes(ctypes.byref(st), L, nex)
+    if ws is None or ws.numel() < per * nc:
+        ws = _workspace(per * nc, ops.coef.device)
+    stats = (scsf_stats * max(nq, 1))()
+    ld_host = evecs_host.shape[2] if evecs_host is not None else 0
+    code = lib.scsf_solve_chains_host(ctypes.byref(st), queue.ctypes.data_as(ctypes.c_void_p),
+                                      starts.ctypes.data_as(ctypes.c_void_p), nc, L, nex, degree, tol, max_iter,
+                                      ctypes.c_uint64(seed), ctypes.c_void_p(evals_host.data_ptr()),
+                                      ctypes.c_void_p(evecs_host.data_ptr()) if evecs_host is not None else None,
+                                      ld_host, stats, _ptr(ws), ws.numel(), _stream())
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return [stats[i].as_dict() for i in range(nq)]
 
 
 # ------------------------------------------------------- component entries ----

@@ -266,3 +266,23 @@ def test_solve_chains_more_chains_than_operators(lib):
     ops, _ = device_problem(f)
     ev, vec, st = lib.solve_chains(ops, [2, 0, 1], 8, cfg.L, cfg.nex, seed=1)
     assert all(s["status"] == 0 and s["warm"] == 0 for s in st)
+
+
+def test_solve_chains_host_streams_identical_results(lib):
+    """scsf_solve_chains_host (pairs streamed to pinned host memory while the chains run) returns
+    exactly what scsf_solve_chains leaves on the device."""
+    import torch
+    cfg = synth.get_config("C1")
+    f = synth.make_batch(cfg, 24)
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    ev, vec, st = lib.solve_chains(ops, perm, 5, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=21)
+    he = torch.empty((len(perm), cfg.L), dtype=torch.float64).pin_memory()
+    hv = torch.zeros((len(perm), cfg.L, f.n + 3), dtype=torch.float64).pin_memory()
+    st2 = lib.solve_chains_host(ops, perm, 5, cfg.L, cfg.nex, he, hv, cfg.degree, cfg.tol, cfg.max_iter, seed=21)
+    assert [s["iterations"] for s in st2] == [s["iterations"] for s in st]
+    assert torch.equal(he, ev.cpu())
+    assert torch.equal(hv[:, :, :f.n], vec[:, :, :f.n].cpu())
+    he2 = torch.empty((len(perm), cfg.L), dtype=torch.float64).pin_memory()
+    lib.solve_chains_host(ops, perm, 5, cfg.L, cfg.nex, he2, None, cfg.degree, cfg.tol, cfg.max_iter, seed=21)
+    assert torch.equal(he2, ev.cpu())
