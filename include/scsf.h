@@ -119,6 +119,29 @@ int scsf_signatures(const double* params, int32_t N, int32_t dim, int32_t p, int
 /* ------------------------------------------------------------ operators ---- */
 
 /*
+ * Coefficient fields of a batch on the device (Fig. 1 steps 1-2,
+ * P:49; the paper gives no GRF recipe, P:759/789/807 — this is DESIGN.md §3's):
+ *   g(x) = sum_{k in {1..K}^dim} xi_k (1 + |k|^2)^(-s) prod_d sin(pi k_d x_d),
+ *   g <- g * sigma / s_K when sigma > 0, s_K = sqrt(sum_k (1+|k|^2)^(-2s) / 2^dim),
+ * at nodes x_i = (i+1) h and face midpoints (i+1/2) h, h = 1/(nx+1); then
+ *   family 0 (diva,  -div(a grad u)):         faces = vscale e^g, c = 0, P0 = vscale e^g(nodes)
+ *   family 1 (lapv,  -Lap u + V u):           faces = 1, c = P0 = vscale e^g(nodes)
+ *   family 2 (divac, -div(a grad u) + c u):   faces = e^{g_a}, P0 = e^{g_a}, c = P1 = e^{g_c}
+ *  xi       dev [n_ops][F][K^dim] standard normal draws (F = 2 for divac, else 1),
+ *           C order [kx][ky](kz) — drawn by the caller, so a batch is reproducible
+ *  faces_*  dev out, layouts as scsf_assemble's inputs; c dev [n_ops][n] out;
+ *  params   dev [n_ops][F][n] out (scsf_sort's parameter matrices)
+ *  ws       dev >= scsf_grf_workspace_bytes(nx, K) (basis tables)
+ * Limits: dim 2: K <= 32; dim 3: K^3 <= 1024 and nx <= 63.
+ * Errors: SCSF_ERR_ARG, SCSF_ERR_WORKSPACE, SCSF_ERR_DEVICE.  Synchronises the stream.
+ */
+size_t scsf_grf_workspace_bytes(int32_t nx, int32_t K);
+int scsf_grf_fields(int32_t dim, int32_t nx, int32_t K, double s, double sigma, double vscale,
+                    int32_t family, int32_t n_ops, const double* xi, double* faces_x,
+                    double* faces_y, double* faces_z, double* c, double* params, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/*
  * Flux-form FD assembly (App. B; reading R20):
  *   A(k,k) = sum of the 2*dim face coefficients around node k / h^2 + c[k],
  *   A(k,k+s_d) = -a(face between k and k+s_d) / h^2.
@@ -227,6 +250,31 @@ int scsf_solve_chains_host(const scsf_ops* ops, const int32_t* queue, const int3
                            int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol,
                            int32_t max_iter, uint64_t seed, double* evals_host, double* evecs_host,
                            int64_t ld_host, scsf_stats* st, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Resumable chains ("per-chain cursor plus the last Ritz block
+ * persisted, so a chain resumes from its last solved operator as a warm start";
+ * warm start P:270-277, "V~_0 = V^(i-1)").  A chain's state after an
+ * operator is what the next operator's warm start reads:
+ *   state = [ theta (b doubles, Ritz values ascending) | V (b x n, column-major, ld = n) ]
+ * scsf_chain_state_doubles returns b * (n + 1) (0 on bad arguments).
+ * scsf_solve_chains_resume is scsf_solve_chains where
+ *  state_in   dev [n_chains][state] or NULL.  Non-NULL: chain c's first operator
+ *             warm-starts from state_in[c] exactly as if it followed, in one call,
+ *             the operator that produced it (inherited bounds included), so a
+ *             queue solved in segments gives bit-identical pairs to one pass.
+ *             NULL: every chain starts cold (seeded random block).
+ *  state_out  dev [n_chains][state] out (required; must not alias state_in): the
+ *             state after each chain's last operator of this call.  A chain with an
+ *             empty slice copies state_in[c] (or writes NaNs when state_in is NULL).
+ * Errors as scsf_solve_chains; SCSF_ERR_ARG when state_out is NULL or aliases state_in.
+ */
+int64_t scsf_chain_state_doubles(const scsf_ops* ops, int32_t L, int32_t nex);
+int scsf_solve_chains_resume(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                             int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol,
+                             int32_t max_iter, uint64_t seed, const double* state_in, double* state_out,
+                             double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /* ------------------------------------------- row-partitioned solve ---- */
 /*

@@ -66,6 +66,11 @@ static int init_kernel_attrs() {
   SCSF_TRY(stencil_init_attrs());
   return SCSF_OK;
 }
+// k_grf.cu
+size_t grf_ws_doubles(int nx, int K);
+int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int family, int n_ops,
+             const double* xi, double* fx, double* fy, double* fz, double* c, double* params, double* tab,
+             cudaStream_t st);
 // k_stencil.cu
 int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
                   const double* c, double* coef, cudaStream_t s);
@@ -176,6 +181,33 @@ int scsf_assemble(const scsf_ops* ops, double h, const double* faces_x, const do
   return SCSF_OK;
 }
 
+size_t scsf_grf_workspace_bytes(int32_t nx, int32_t K) {
+  if (nx < 1 || K < 1) return 0;
+  return grf_ws_doubles(nx, K) * sizeof(double);
+}
+
+int scsf_grf_fields(int32_t dim, int32_t nx, int32_t K, double s, double sigma, double vscale, int32_t family,
+                    int32_t n_ops, const double* xi, double* faces_x, double* faces_y, double* faces_z, double* c,
+                    double* params, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_ARG_CHECK(dim == 2 || dim == 3, "dim must be 2 or 3");
+  SCSF_ARG_CHECK(nx >= 1 && n_ops >= 0, "nx >= 1 and n_ops >= 0 required");
+  SCSF_ARG_CHECK(K >= 1 && (dim == 2 ? K <= 32 : K * K * K <= 1024), "K out of range (2-D: <= 32, 3-D: K^3 <= 1024)");
+  SCSF_ARG_CHECK(dim == 2 || nx + 1 <= 64, "3-D fields need nx <= 63");
+  SCSF_ARG_CHECK(family >= 0 && family <= 2, "family must be 0 (diva), 1 (lapv) or 2 (divac)");
+  SCSF_ARG_CHECK(s >= 0.0 && vscale > 0.0, "s >= 0 and vscale > 0 required");
+  if (n_ops == 0) return SCSF_OK;
+  SCSF_ARG_CHECK(xi && faces_x && faces_y && (dim == 2 || faces_z) && c && params, "NULL array");
+  if (!ws || ws_bytes < grf_ws_doubles(nx, K) * sizeof(double)) {
+    set_error("workspace too small: need %zu bytes", grf_ws_doubles(nx, K) * sizeof(double));
+    return SCSF_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCSF_TRY(grf_impl(dim, nx, K, s, sigma, vscale, family, n_ops, xi, faces_x, faces_y, faces_z, c, params,
+                    (double*)ws, st));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(st));
+  return SCSF_OK;
+}
+
 size_t scsf_filter_workspace_bytes(const scsf_ops* ops, int32_t k, int64_t ldy) {
   if (!ops || k < 1) return 0;
   Arena a(nullptr, 0);
@@ -279,7 +311,16 @@ struct HostSink {
 
 static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain, int32_t L, int32_t nex,
                      int32_t degree, double tol, int32_t max_iter, uint64_t seed, double* evals, double* evecs,
-                     int64_t ld_vec, scsf_stats* st, SolveWS& w, cudaStream_t s, HostSink* sink = nullptr) {
+                     int64_t ld_vec, scsf_stats* st, SolveWS& w, cudaStream_t s, HostSink* sink = nullptr,
+                     const double* state_in = nullptr, double* state_out = nullptr) {
+  const int bb = L + nex;
+  if (state_in) {   // resume: the block and Ritz values of the operator solved before chain[0]
+    SCSF_CUDA_CHECK(cudaMemcpyAsync(w.theta_sorted, state_in, bb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SCSF_CUDA_CHECK(cudaMemcpy2DAsync(w.V, w.ldv * sizeof(double), state_in + bb, w.n * sizeof(double),
+                                      w.n * sizeof(double), bb, cudaMemcpyDeviceToDevice, s));
+    if (w.ldv > w.n)
+      SCSF_CUDA_CHECK(cudaMemset2DAsync(w.V + w.n, w.ldv * sizeof(double), 0, (w.ldv - w.n) * sizeof(double), bb, s));
+  }
   cudaStream_t cs = nullptr;
   cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
   if (sink) {
@@ -302,8 +343,8 @@ static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   int worst = SCSF_OK;
   for (int k = 0; k < n_chain; ++k) {
     scsf_stats local{};
-    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0, false, seed + (uint64_t)chain[k], w,
-                       &local, s);
+    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0 || state_in != nullptr, false,
+                       seed + (uint64_t)chain[k], w, &local, s);
     if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
     if (r > worst) worst = r;
     if (st) st[k] = local;
@@ -332,6 +373,11 @@ static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
                                           cudaMemcpyDeviceToHost, cs));
       SCSF_CUDA_CHECK(cudaEventRecord(done[b], cs));
     }
+  }
+  if (state_out && n_chain > 0) {
+    SCSF_CUDA_CHECK(cudaMemcpyAsync(state_out, w.theta_sorted, bb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SCSF_CUDA_CHECK(cudaMemcpy2DAsync(state_out + bb, w.n * sizeof(double), w.V, w.ldv * sizeof(double),
+                                      w.n * sizeof(double), bb, cudaMemcpyDeviceToDevice, s));
   }
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
   return worst;
@@ -373,11 +419,30 @@ int scsf_solve_queue(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   return r;
 }
 
+static int64_t state_doubles(const scsf_ops* ops, int L, int nex) {
+  return (int64_t)(L + nex) * (1 + (int64_t)ops->nx * ops->ny * ops->nz);
+}
+
 static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
                              int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
                              uint64_t seed, double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws,
                              size_t ws_bytes, void* stream, double* evals_host, double* evecs_host,
-                             int64_t ld_host);
+                             int64_t ld_host, const double* state_in = nullptr, double* state_out = nullptr);
+
+int64_t scsf_chain_state_doubles(const scsf_ops* ops, int32_t L, int32_t nex) {
+  if (!ops || L < 1 || nex < 0) return 0;
+  return state_doubles(ops, L, nex);
+}
+
+int scsf_solve_chains_resume(const scsf_ops* ops, const int32_t* queue, const int32_t* chain_start,
+                             int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
+                             uint64_t seed, const double* state_in, double* state_out, double* evals, double* evecs,
+                             int64_t ld_vec, scsf_stats* st, void* ws, size_t ws_bytes, void* stream) {
+  SCSF_ARG_CHECK(state_out != nullptr, "state_out is NULL");
+  SCSF_ARG_CHECK(state_in != state_out, "state_in and state_out must not alias");
+  return solve_chains_impl(ops, queue, chain_start, n_chains, L, nex, degree, tol, max_iter, seed, evals, evecs,
+                           ld_vec, st, ws, ws_bytes, stream, nullptr, nullptr, 0, state_in, state_out);
+}
 
 static size_t sink_bytes(const scsf_ops* ops, int L) {
   const int64_t ldv = round_up((int64_t)ops->nx * ops->ny * ops->nz, 32);
@@ -412,7 +477,7 @@ static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const in
                              int32_t n_chains, int32_t L, int32_t nex, int32_t degree, double tol, int32_t max_iter,
                              uint64_t seed, double* evals, double* evecs, int64_t ld_vec, scsf_stats* st, void* ws,
                              size_t ws_bytes, void* stream, double* evals_host, double* evecs_host,
-                             int64_t ld_host) {
+                             int64_t ld_host, const double* state_in, double* state_out) {
   const bool to_host = evals_host != nullptr;
   SCSF_TRY(check_solve_args(ops, L, nex, degree, tol, max_iter));
   SCSF_ARG_CHECK(n_chains >= 1 && chain_start != nullptr, "n_chains >= 1 and chain_start required");
@@ -421,7 +486,7 @@ static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const in
     SCSF_ARG_CHECK(chain_start[c + 1] >= chain_start[c], "chain_start must be non-decreasing");
   const int32_t len = chain_start[n_chains];
   SCSF_TRY(check_queue(ops, queue, len, to_host ? evals_host : evals, evecs, ld_vec));
-  if (len == 0) return SCSF_OK;
+  if (len == 0 && !state_out) return SCSF_OK;
   const size_t per_solve = solve_ws_bytes(ops, L, nex);
   const size_t per = per_solve + (to_host ? sink_bytes(ops, L) : 0);
   if (!ws || ws_bytes < per * (size_t)n_chains) {
@@ -461,10 +526,21 @@ static int solve_chains_impl(const scsf_ops* ops, const int32_t* queue, const in
       sink.evecs = evecs_host ? evecs_host + (int64_t)b0 * L * ld_host : nullptr;
       sink.ld = ld_host;
     }
+    const int64_t sd = state_doubles(ops, L, nex);
+    const double* sin_c = state_in ? state_in + sd * c : nullptr;
+    double* sout_c = state_out ? state_out + sd * c : nullptr;
     if (r == SCSF_OK && cnt > 0)
       r = run_chain(ops, queue + b0, cnt, L, nex, degree, tol, max_iter, seed,
                     evals ? evals + (int64_t)b0 * L : nullptr, evecs ? evecs + (int64_t)b0 * L * ld_vec : nullptr,
-                    ld_vec, st ? st + b0 : nullptr, w, s, to_host ? &sink : nullptr);
+                    ld_vec, st ? st + b0 : nullptr, w, s, to_host ? &sink : nullptr, sin_c, sout_c);
+    else if (r == SCSF_OK && sout_c && sout_c != sin_c) {   // an empty slice carries its state through
+      cudaError_t e = sin_c ? cudaMemcpyAsync(sout_c, sin_c, sd * sizeof(double), cudaMemcpyDeviceToDevice, s)
+                            : cudaMemsetAsync(sout_c, 0xff, sd * sizeof(double), s);   // NaN: no state
+      if (e != cudaSuccess) {
+        r = SCSF_ERR_DEVICE;
+        set_error("state copy: %s", cudaGetErrorString(e));
+      }
+    }
     status[c] = r;
     if (r != SCSF_OK) msg[c] = scsf_last_error();
     cudaStreamSynchronize(s);

@@ -171,3 +171,118 @@ def gather_slabs(evecs_local: torch.Tensor, nx: int, rows: tuple[int, int], ny: 
     got = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(got, pad)
     return torch.cat([g[:, :, :nx * (b - a)] for g, (a, b) in zip(got, parts)], dim=2)
+
+
+# ------------------------------------------------------------ resumable run ----
+# SURVEY f4 / §3 "checkpoint / resume": per-chain cursor plus the last Ritz block persisted, so
+# an interrupted dataset run resumes from each chain's last solved operator as a warm start
+# (P:270-277).  Every chain's slice of the sorted queue is cut into segments of `segment`
+# operators; one call of scsf_solve_chains_resume advances every chain by one segment.  After a
+# segment the pairs land in memory-mapped .npy files (by queue position), then the chain states
+# go to state_<j>.npy and finally manifest.json's cursor moves to j (each file written to a
+# temporary name and renamed), so a crash at any point leaves a consistent checkpoint.
+def segment_plan(chain_start, segment: int):
+    """[(queue positions of segment j, chain_start of segment j)] for contiguous chains."""
+    cs = np.asarray(chain_start, dtype=np.int64)
+    if segment < 1:
+        raise ValueError("segment must be >= 1")
+    nc = len(cs) - 1
+    n_seg = int(max(((cs[c + 1] - cs[c] + segment - 1) // segment for c in range(nc)), default=0))
+    plan = []
+    for j in range(n_seg):
+        pos, starts = [], [0]
+        for c in range(nc):
+            lo = min(int(cs[c]) + j * segment, int(cs[c + 1]))
+            hi = min(lo + segment, int(cs[c + 1]))
+            pos.extend(range(lo, hi))
+            starts.append(starts[-1] + hi - lo)
+        plan.append((np.asarray(pos, dtype=np.int64), np.asarray(starts, dtype=np.int32)))
+    return plan
+
+
+def _atomic_write(path, write):
+    """write(file object) to path.tmp, fsync, then rename over path."""
+    import os
+    tmp = f"{path}.tmp"
+    with open(tmp, "wb") as fh:
+        write(fh)
+        fh.flush()
+        os.fsync(fh.fileno())
+    os.replace(tmp, path)
+
+
+def run_resumable(ops, queue, n_chains: int, sp: SolveParams, out_dir: str, segment: int = 8,
+                  want_vecs: bool = False, max_segments: int | None = None, solve_fn=None,
+                  state_doubles: int | None = None, n: int | None = None, device=None):
+    """Solve the sorted `queue` as n_chains warm-start chains, checkpointing to `out_dir` after
+    every segment; a later call with the same arguments continues where the last one stopped.
+
+    Output files (queue position order): evals.npy [N, L], stats.npy [N, 3] (status,
+    iterations, max_rel_resid), evecs.npy [N, L, n] when want_vecs, state_<j>.npy, manifest.json.
+    max_segments: stop after that many segments in this call (an interruption, for tests).
+    solve_fn / state_doubles / n / device: injection points for host-only tests; default is
+    scsf.solve_chains_resume on ops' device.
+    Returns (segments done, total segments)."""
+    import json
+    import os
+    queue = np.asarray(queue, dtype=np.int32)
+    N = int(queue.shape[0])
+    starts = scsf.split_chains(N, n_chains)
+    nc = len(starts) - 1
+    plan = segment_plan(starts, segment)
+    solve_fn = solve_fn or scsf.solve_chains_resume
+    if device is None:
+        device = ops.coef.device
+    n = ops.nx * ops.ny * ops.nz if n is None else n
+    sd = scsf.chain_state_doubles(ops, sp.L, sp.nex) if state_doubles is None else state_doubles
+    os.makedirs(out_dir, exist_ok=True)
+    man_path = os.path.join(out_dir, "manifest.json")
+    key = {"N": N, "L": sp.L, "nex": sp.nex, "n": int(n), "n_chains": nc, "segment": int(segment),
+           "degree": sp.degree, "tol": sp.tol, "max_iter": sp.max_iter, "seed": sp.seed, "want_vecs": bool(want_vecs),
+           "queue_crc": int(np.bitwise_xor.reduce(queue.astype(np.int64) * (1 + np.arange(N, dtype=np.int64))))
+           if N else 0}
+    fmm = np.lib.format.open_memmap
+    if os.path.exists(man_path):
+        man = json.load(open(man_path))
+        if man["key"] != key:
+            raise ValueError(f"{out_dir} holds a checkpoint of a different run: {man['key']} != {key}")
+        cursor = int(man["cursor"])
+        ev = fmm(os.path.join(out_dir, "evals.npy"), mode="r+")
+        sts = fmm(os.path.join(out_dir, "stats.npy"), mode="r+")
+        vec = fmm(os.path.join(out_dir, "evecs.npy"), mode="r+") if want_vecs else None
+    else:
+        cursor = 0
+        ev = fmm(os.path.join(out_dir, "evals.npy"), mode="w+", dtype=np.float64, shape=(N, sp.L))
+        sts = fmm(os.path.join(out_dir, "stats.npy"), mode="w+", dtype=np.float64, shape=(N, 3))
+        vec = (fmm(os.path.join(out_dir, "evecs.npy"), mode="w+", dtype=np.float64, shape=(N, sp.L, n))
+               if want_vecs else None)
+    state = None
+    if cursor > 0:
+        state = torch.from_numpy(np.load(os.path.join(out_dir, f"state_{cursor}.npy"))).to(device)
+    done_now = 0
+    for j in range(cursor, len(plan)):
+        if max_segments is not None and done_now >= max_segments:
+            break
+        pos, seg_starts = plan[j]
+        state_out = torch.empty((nc, sd), dtype=torch.float64, device=device)
+        evals, evecs, stats = solve_fn(ops, queue[pos], seg_starts, sp.L, sp.nex, state, state_out,
+                                       degree=sp.degree, tol=sp.tol, max_iter=sp.max_iter, seed=sp.seed,
+                                       want_vecs=want_vecs, raise_on_fail=False)
+        ev[pos] = evals.cpu().numpy()
+        sts[pos] = np.array([[s["status"], s["iterations"], s["max_rel_resid"]] for s in stats]).reshape(-1, 3)
+        if want_vecs:
+            vec[pos] = evecs[:, :, :n].cpu().numpy()
+            vec.flush()
+        ev.flush()
+        sts.flush()
+        host_state = state_out.cpu().numpy()
+        _atomic_write(os.path.join(out_dir, f"state_{j + 1}.npy"),
+                      lambda fh: np.save(fh, host_state))
+        _atomic_write(man_path, lambda fh: fh.write(json.dumps({"key": key, "cursor": j + 1,
+                                                                "segments": len(plan)}).encode()))
+        if j > 0 and os.path.exists(os.path.join(out_dir, f"state_{j}.npy")):
+            os.remove(os.path.join(out_dir, f"state_{j}.npy"))
+        state = state_out
+        cursor = j + 1
+        done_now += 1
+    return cursor, len(plan)

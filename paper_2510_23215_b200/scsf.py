@@ -30,6 +30,7 @@ EXPORTED = [
     "scsf_comm_unique_id", "scsf_comm_create", "scsf_comm_create_loopback", "scsf_comm_destroy",
     "scsf_comm_rank", "scsf_slab_rows", "scsf_solve_dist_workspace_bytes", "scsf_solve_queue_dist",
     "scsf_filter_kind", "scsf_solve_chains_host_workspace_bytes", "scsf_solve_chains_host",
+    "scsf_chain_state_doubles", "scsf_solve_chains_resume", "scsf_grf_workspace_bytes", "scsf_grf_fields",
 ]
 
 
@@ -103,6 +104,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "scsf_solve_chains_host_workspace_bytes": (SZ, [OPS, I32, I32]),
         "scsf_solve_chains_host": (ctypes.c_int, [OPS, P, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P, I64,
                                                   ST, P, SZ, P]),
+        "scsf_chain_state_doubles": (I64, [OPS, I32, I32]),
+        "scsf_grf_workspace_bytes": (SZ, [I32, I32]),
+        "scsf_grf_fields": (ctypes.c_int, [I32, I32, I32, D, D, D, I32, I32, P, P, P, P, P, P, P, SZ, P]),
+        "scsf_solve_chains_resume": (ctypes.c_int, [OPS, P, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P,
+                                                    P, P, I64, ST, P, SZ, P]),
         "scsf_comm_unique_id": (ctypes.c_int, [P]),
         "scsf_comm_create": (ctypes.c_int, [I32, I32, P, ctypes.POINTER(P)]),
         "scsf_comm_create_loopback": (ctypes.c_int, [I32, P]),
@@ -208,6 +214,36 @@ def assemble(dim: int, nx: int, h: float, faces, c: torch.Tensor | None) -> Oper
     _check(lib.scsf_assemble(ctypes.byref(st), h, _ptr(faces[0]), _ptr(faces[1]), _ptr(fz), _ptr(c),
                              _ptr(coef), _stream()))
     return ops
+
+
+GRF_FAMILIES = {"diva": 0, "lapv": 1, "divac": 2}
+
+
+def grf_fields(dim: int, nx: int, K: int, s: float, sigma: float | None, vscale: float, family: str,
+               xi: torch.Tensor):
+    """Coefficient arrays of a batch from its normal draws, on the device (scsf_grf_fields).
+    xi: cuda float64 [N, F, K^dim].  Returns (faces list, c [N, n], params [N, F, n])."""
+    lib = load_library()
+    _require_cuda_f64(xi, "xi")
+    fam = GRF_FAMILIES[family]
+    F = 2 if fam == 2 else 1
+    N = xi.shape[0]
+    if xi.shape[1:] != (F, K ** dim):
+        raise ValueError(f"xi must be [N, {F}, {K ** dim}]")
+    n = nx ** dim
+    dev = xi.device
+    faces = []
+    for ax in range(dim):
+        shp = [nx] * dim
+        shp[dim - 1 - ax] = nx + 1
+        faces.append(torch.empty((N, *shp), dtype=torch.float64, device=dev))
+    c = torch.empty((N, n), dtype=torch.float64, device=dev)
+    params = torch.empty((N, F, n), dtype=torch.float64, device=dev)
+    ws = _workspace(lib.scsf_grf_workspace_bytes(nx, K), dev)
+    _check(lib.scsf_grf_fields(dim, nx, K, s, -1.0 if sigma is None else sigma, vscale, fam, N, _ptr(xi),
+                               _ptr(faces[0]), _ptr(faces[1]), _ptr(faces[2]) if dim == 3 else None, _ptr(c),
+                               _ptr(params), _ptr(ws), ws.numel(), _stream()))
+    return faces, c, params
 
 
 # ----------------------------------------------------------------------- sort ----
@@ -374,6 +410,45 @@ def solve_chains_host(ops: Operators, queue, n_chains: int, L: int, nex: int, ev
     if raise_on_fail or code != SCSF_ERR_NUMERICAL:
         _check(code)
     return [stats[i].as_dict() for i in range(nq)]
+
+
+def chain_state_doubles(ops: Operators, L: int, nex: int) -> int:
+    """Length of one chain's resume state: b * (n + 1) doubles (scsf_chain_state_doubles)."""
+    st = ops.c_struct()
+    return int(load_library().scsf_chain_state_doubles(ctypes.byref(st), L, nex))
+
+
+def solve_chains_resume(ops: Operators, queue, chain_start, L: int, nex: int, state_in: torch.Tensor | None,
+                        state_out: torch.Tensor, degree: int = 20, tol: float = 1e-8, max_iter: int = 200,
+                        seed: int = 0, want_vecs: bool = False, raise_on_fail=True, ws: torch.Tensor | None = None):
+    """scsf_solve_chains_resume: chains over queue[chain_start[c]:chain_start[c+1]], chain c warm from
+    state_in[c] (or cold when state_in is None); state_out [n_chains, state] receives each chain's
+    state after its last operator.  Returns (evals[len, L], evecs or None, stats list)."""
+    lib = load_library()
+    queue = np.ascontiguousarray(np.asarray(queue, dtype=np.int32))
+    starts = np.ascontiguousarray(np.asarray(chain_start, dtype=np.int32))
+    nq, nc = int(queue.shape[0]), len(starts) - 1
+    sd = chain_state_doubles(ops, L, nex)
+    for t, nm in ((state_in, "state_in"), (state_out, "state_out")):
+        if t is not None:
+            _require_cuda_f64(t, nm)
+            if t.numel() < nc * sd:
+                raise ValueError(f"{nm} needs {nc} x {sd} doubles")
+    st = ops.c_struct()
+    per = lib.scsf_solve_workspace_bytes(ctypes.byref(st), L, nex)
+    if ws is None or ws.numel() < per * nc:
+        ws = _workspace(per * nc, ops.coef.device)
+    dev = ops.coef.device
+    evals = torch.empty((max(nq, 1), L), dtype=torch.float64, device=dev)
+    evecs = torch.empty((nq, L, ops.ld), dtype=torch.float64, device=dev) if want_vecs else None
+    stats = (scsf_stats * max(nq, 1))()
+    code = lib.scsf_solve_chains_resume(ctypes.byref(st), queue.ctypes.data_as(ctypes.c_void_p),
+                                        starts.ctypes.data_as(ctypes.c_void_p), nc, L, nex, degree, tol, max_iter,
+                                        ctypes.c_uint64(seed), _ptr(state_in), _ptr(state_out), _ptr(evals),
+                                        _ptr(evecs), ops.ld, stats, _ptr(ws), ws.numel(), _stream())
+    if raise_on_fail or code != SCSF_ERR_NUMERICAL:
+        _check(code)
+    return evals[:nq], evecs, [stats[i].as_dict() for i in range(nq)]
 
 
 # ------------------------------------------------------- component entries ----

@@ -101,6 +101,21 @@ def _xi(cfg_index: int, i: int, f: int, K: int, dim: int) -> np.ndarray:
     return rng.standard_normal((K,) * dim)
 
 
+def draw_xi(cfg: Config, n_ops: int | None = None, start: int = 0, indices=None) -> np.ndarray:
+    """The normal draws of operators start..start+n_ops-1 (or `indices`): [N, F, K^dim], C order
+    per field — the input of the device-side field evaluation (scsf_grf_fields); make_batch
+    evaluates the same draws on the host."""
+    if indices is None:
+        N = cfg.n_ops if n_ops is None else n_ops
+        indices = range(start, start + N)
+    ci = _CFG_INDEX.get(cfg.name, 0)
+    out = np.empty((len(indices), cfg.fields, cfg.K ** cfg.dim))
+    for j, i in enumerate(indices):
+        for f in range(cfg.fields):
+            out[j, f] = _xi(ci, int(i), f, cfg.K, cfg.dim).reshape(-1)
+    return out
+
+
 def make_fields(cfg: Config, i: int, f: int, cfg_index: int | None = None):
     """One GRF sample (operator i, field f) -> (nodal g, [face g per axis])."""
     ci = _CFG_INDEX.get(cfg.name, 0) if cfg_index is None else cfg_index
