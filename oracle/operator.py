@@ -17,11 +17,45 @@ with face-midpoint coefficients, the sign making A positive definite:
 
 For a == 1, c == 0 this is -(Kronecker sum of App. B's tridiag(1,-2,1)/h^2),
 i.e. h^2 A = -M_Eq2 on the paper's 2x2 example (pinned in tests).
+
+Vibration family (SURVEY f3; PAPER.md:793-807, thin plate  Lap(D Lap u) = lambda rho u;
+SPEC discretize "vibration"; reading R25): with Lh the 5-point Dirichlet
+Laplacian  (Lh u)_k = (4 u_k - sum of the 4 neighbours) / h^2  (= -Lap_h, SPD),
+  A_bih = Lh diag(D) Lh      (13-point, symmetric: Lh is symmetric),
+  B     = diag(rho)^(-1/2) A_bih diag(rho)^(-1/2),
+the standard form of the pencil (A_bih, diag(rho)): same eigenvalues, eigenvectors
+y = diag(rho)^(1/2) u.  Both products are formed literally with scipy.sparse, then
+(B + B^T)/2 removes the last-ulp asymmetry of the products' summation order.
 """
 from __future__ import annotations
 
 import numpy as np
 import scipy.sparse as sp
+
+
+def _is_vib(fields) -> bool:
+    return getattr(fields, "family", "flux") == "vib"
+
+
+def laplacian_csr(nx: int, h: float) -> sp.csr_matrix:
+    """Lh = -Lap_h on the nx x nx interior grid, Dirichlet, x fastest: kron sum of tridiag(-1, 2, -1)/h^2
+    (App. B P:651-710's 1-D matrix, negated)."""
+    T = sp.diags([-np.ones(nx - 1), 2.0 * np.ones(nx), -np.ones(nx - 1)], [-1, 0, 1]) / (h * h)
+    I = sp.identity(nx)
+    return (sp.kron(I, T) + sp.kron(T, I)).tocsr()
+
+
+def vibration_csr(fields, i) -> sp.csr_matrix:
+    """B = diag(rho)^-1/2 Lh diag(D) Lh diag(rho)^-1/2 of operator i (D = params[i,0], rho = params[i,1])."""
+    D = np.asarray(fields.params[i, 0], dtype=np.float64)
+    rho = np.asarray(fields.params[i, 1], dtype=np.float64)
+    Lh = laplacian_csr(fields.nx, fields.h)
+    A = Lh @ sp.diags(D) @ Lh
+    S = sp.diags(1.0 / np.sqrt(rho))
+    B = (S @ A @ S).tocsr()
+    # symmetric in exact arithmetic; the sparse products sum the two paths of an (i, i+nx+-1)
+    # entry in either order, so average with the transpose for exact symmetry (SPEC invariant)
+    return ((B + B.T) * 0.5).tocsr()
 
 
 def _face_arrays(fields, i):
@@ -33,6 +67,15 @@ def stencil(fields, i):
 
     off_d[k] = A[k, k + stride_d] (zero where the neighbour is outside the grid).
     """
+    if _is_vib(fields):
+        B = vibration_csr(fields, i)
+        n = B.shape[0]
+        offs = []
+        for st in strides(fields):
+            o = np.zeros(n)
+            o[:n - st] = B.diagonal(st)
+            offs.append(o)
+        return B.diagonal(0).copy(), offs
     dim, nx, h = fields.dim, fields.nx, fields.h
     inv_h2 = 1.0 / (h * h)
     faces = _face_arrays(fields, i)
@@ -60,11 +103,15 @@ def stencil(fields, i):
 
 def strides(fields):
     nx = fields.nx
+    if _is_vib(fields):
+        return [1, 2, nx - 1, nx, nx + 1, 2 * nx]
     return [1, nx] if fields.dim == 2 else [1, nx, nx * nx]
 
 
 def assemble_csr(fields, i) -> sp.csr_matrix:
     """Explicit sparse symmetric A^(i)."""
+    if _is_vib(fields):
+        return vibration_csr(fields, i)
     n = fields.n
     diag, offs = stencil(fields, i)
     rows, cols, vals = [np.arange(n)], [np.arange(n)], [diag]

@@ -16,7 +16,8 @@ class Config:
     nx: int                  # interior grid points per axis (ny = nz = nx)
     n_ops: int               # N, operators in the batch
     L: int                   # wanted eigenpairs
-    family: str              # "diva" (-div(a grad u)), "lapv" (-Lap u + V u), "divac" (-div(a grad u) + c u)
+    family: str              # "diva" (-div(a grad u)), "lapv" (-Lap u + V u), "divac" (-div(a grad u) + c u),
+                             # "vib" (thin plate: Lap(D Lap u) = lambda rho u, standard form)
     K: int                   # GRF modes per axis
     s: float                 # GRF spectral decay exponent: (1+|k|^2)^(-s)
     sigma: float | None      # target domain-RMS std of g (None: raw series)
@@ -46,7 +47,7 @@ class Config:
     @property
     def fields(self) -> int:
         """F: number of parameter fields per operator used by the sort."""
-        return 2 if self.family == "divac" else 1
+        return 2 if self.family in ("divac", "vib") else 1
 
     def with_(self, **kw) -> "Config":
         return replace(self, **kw)
@@ -65,7 +66,14 @@ CONFIGS = {
     "C5": Config("C5", 2, 500, 64, 300, "lapv", K=32, s=1.0, sigma=0.5, chains=1),
 }
 
+# SURVEY §8(f) f3, beyond BASELINE.json's five configs: the paper's fourth dataset, thin-plate
+# vibration Lap(D Lap u) = lambda rho u, D and rho lognormal GRF fields
+# ("derived using GRF"), n = 10^4 as the paper's largest comparison.
+EXTRA_CONFIGS = {
+    "V1": Config("V1", 2, 100, 200, 50, "vib", K=8, s=1.0, sigma=0.3, chains=8),
+}
+
 
 def get_config(name: str, **overrides) -> Config:
-    cfg = CONFIGS[name]
+    cfg = CONFIGS[name] if name in CONFIGS else EXTRA_CONFIGS[name]
     return cfg.with_(**overrides) if overrides else cfg

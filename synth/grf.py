@@ -24,9 +24,9 @@ from __future__ import annotations
 from dataclasses import dataclass
 import numpy as np
 
-from .configs import Config, CONFIGS
+from .configs import Config, CONFIGS, EXTRA_CONFIGS
 
-_CFG_INDEX = {name: i for i, name in enumerate(CONFIGS)}
+_CFG_INDEX = {name: i for i, name in enumerate(list(CONFIGS) + list(EXTRA_CONFIGS))}
 
 
 def grf_std(K: int, s: float, dim: int) -> float:
@@ -72,6 +72,8 @@ class OperatorFields:
       2-D: faces[0] [N, ny, nx+1], faces[1] [N, ny+1, nx]
       3-D: faces[0] [N, nz, ny, nx+1], faces[1] [N, nz, ny+1, nx], faces[2] [N, nz+1, ny, nx]
     c: nodal reaction [N, n] (x fastest).  params: sort fields [N, F, n] (x fastest).
+    Vibration family (family == "vib"): no faces and c == 0; the nodal
+    rigidity D and density rho are params[:, 0] and params[:, 1].
     """
     dim: int
     nx: int
@@ -79,6 +81,11 @@ class OperatorFields:
     faces: list
     c: np.ndarray
     params: np.ndarray
+    family: str = "flux"
+
+    @property
+    def is_vib(self) -> bool:
+        return self.family == "vib"
 
     @property
     def n_ops(self) -> int:
@@ -93,7 +100,7 @@ class OperatorFields:
         return OperatorFields(self.dim, self.nx, self.h,
                               [np.ascontiguousarray(f[idx]) for f in self.faces],
                               np.ascontiguousarray(self.c[idx]),
-                              np.ascontiguousarray(self.params[idx]))
+                              np.ascontiguousarray(self.params[idx]), self.family)
 
 
 def _xi(cfg_index: int, i: int, f: int, K: int, dim: int) -> np.ndarray:
@@ -158,6 +165,13 @@ def make_batch(cfg: Config, n_ops: int | None = None, start: int = 0, indices=No
         s[dim - 1 - ax] = nx + 1                        # C order: axis x is last
         face_shapes.append(tuple(s))
     nf = 0 if params_only else N
+    if cfg.family == "vib":
+        params = np.empty((N, 2, n))
+        for j, i in enumerate(indices):
+            for f in range(2):
+                g_node, _ = make_fields(cfg, i, f)
+                params[j, f] = np.exp(g_node).reshape(n)
+        return OperatorFields(dim, nx, cfg.h, [], np.zeros((nf, n)), params, "vib")
     faces = [np.empty((nf,) + fs) for fs in face_shapes]
     c = np.zeros((nf, n))
     params = np.empty((N, cfg.fields, n))
