@@ -60,10 +60,27 @@ typedef struct {
   int32_t dim;          /* 2 or 3                                        */
   int32_t nx, ny, nz;   /* interior grid size (nz = 1 when dim == 2)     */
   int32_t n_ops;        /* operators in the batch                        */
-  int32_t reserved;     /* must be 0                                     */
+  int32_t stencil;      /* SCSF_STENCIL_FLUX (0) or SCSF_STENCIL_VIB13 (1) */
   int64_t ld;           /* stride between coefficient arrays (doubles)   */
-  const double* coef;   /* dev [n_ops][1+dim][ld]                        */
+  const double* coef;   /* dev [n_ops][scsf_ncoef][ld]                   */
 } scsf_ops;
+
+/*
+ * Stencil kinds.  SCSF_STENCIL_FLUX: the layout above, 1 + dim arrays.
+ * SCSF_STENCIL_VIB13 (dim 2 only): the standard form B of the thin-plate
+ * vibration pencil (reading R25; scsf_assemble_vibration), a
+ * symmetric 13-point stencil in 7 arrays, k = ix + nx*iy:
+ *   coef[(i*7 + 0)*ld + k] = B(k, k)
+ *   coef[(i*7 + 1)*ld + k] = B(k, k+1)       (0 when ix = nx-1)
+ *   coef[(i*7 + 2)*ld + k] = B(k, k+2)       (0 when ix >= nx-2)
+ *   coef[(i*7 + 3)*ld + k] = B(k, k+nx-1)    (0 when ix = 0 or iy = ny-1)
+ *   coef[(i*7 + 4)*ld + k] = B(k, k+nx)      (0 when iy = ny-1)
+ *   coef[(i*7 + 5)*ld + k] = B(k, k+nx+1)    (0 when ix = nx-1 or iy = ny-1)
+ *   coef[(i*7 + 6)*ld + k] = B(k, k+2nx)     (0 when iy >= ny-2)
+ * The filter runs the per-step streaming stencil for this kind, and the
+ * row-partitioned solve (scsf_solve_queue_dist) does not support it.
+ */
+enum { SCSF_STENCIL_FLUX = 0, SCSF_STENCIL_VIB13 = 1 };
 
 /* Per-operator statistics (SPEC S:384-388 SolveRecord fields; P:463-479 Tab. sort1). */
 typedef struct {
@@ -119,6 +136,23 @@ int scsf_signatures(const double* params, int32_t N, int32_t dim, int32_t p, int
 /* ------------------------------------------------------------ operators ---- */
 
 /*
+ * Thin-plate vibration operators ("Lap(D Lap u) =
+ * lambda rho u", reading R25):  B = diag(rho)^-1/2 Lh diag(D) Lh diag(rho)^-1/2,
+ * Lh the 5-point Dirichlet -Lap_h (4 u_k - neighbours)/h^2, so per entry
+ *   h^4 sqrt(rho_k rho_l) B(k,l) = 16 D_k + sum of D over k's in-grid x/y neighbours   (l = k)
+ *                              = -4 (D_k + D_l)                 (l = k+1 or k+nx, same row / column)
+ *                              = D_m                            (l = k+2 or k+2nx, m the point between)
+ *                              = D of the two common neighbours (l = k+nx+-1, diagonal)
+ * ops->stencil must be SCSF_STENCIL_VIB13, ops->dim 2.
+ *  D, rho  dev, operator i's nodal fields at D + i*field_stride, rho + i*field_stride
+ *          (x fastest; field_stride >= n; both > 0 — e.g. params [N][2][n] with
+ *          rho = params + n and field_stride = 2n)
+ *  coef_out dev [n_ops][7][ld]; pads k >= n with 0.
+ */
+int scsf_assemble_vibration(const scsf_ops* ops, double h, const double* D, const double* rho,
+                            int64_t field_stride, double* coef_out, void* stream);
+
+/*
  * Coefficient fields of a batch on the device (Fig. 1 steps 1-2,
  * P:49; the paper gives no GRF recipe, P:759/789/807 — this is DESIGN.md §3's):
  *   g(x) = sum_{k in {1..K}^dim} xi_k (1 + |k|^2)^(-s) prod_d sin(pi k_d x_d),
@@ -127,7 +161,9 @@ int scsf_signatures(const double* params, int32_t N, int32_t dim, int32_t p, int
  *   family 0 (diva,  -div(a grad u)):         faces = vscale e^g, c = 0, P0 = vscale e^g(nodes)
  *   family 1 (lapv,  -Lap u + V u):           faces = 1, c = P0 = vscale e^g(nodes)
  *   family 2 (divac, -div(a grad u) + c u):   faces = e^{g_a}, P0 = e^{g_a}, c = P1 = e^{g_c}
- *  xi       dev [n_ops][F][K^dim] standard normal draws (F = 2 for divac, else 1),
+ *   family 3 (vib, Lap(D Lap u) = l rho u):   P0 = D = e^{g_0}, P1 = rho = e^{g_1}; faces, c unused
+ *                                             (may be NULL; feed P to scsf_assemble_vibration)
+ *  xi       dev [n_ops][F][K^dim] standard normal draws (F = 2 for divac / vib, else 1),
  *           C order [kx][ky](kz) — drawn by the caller, so a batch is reproducible
  *  faces_*  dev out, layouts as scsf_assemble's inputs; c dev [n_ops][n] out;
  *  params   dev [n_ops][F][n] out (scsf_sort's parameter matrices)

@@ -72,6 +72,8 @@ int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int 
              const double* xi, double* fx, double* fy, double* fz, double* c, double* params, double* tab,
              cudaStream_t st);
 // k_stencil.cu
+int assemble_vib_impl(const scsf_ops* ops, double h, const double* D, const double* rho, int64_t fstride,
+                      double* coef, cudaStream_t s);
 int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
                   const double* c, double* coef, cudaStream_t s);
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
@@ -97,6 +99,11 @@ static int check_ops(const scsf_ops* ops) {
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
   SCSF_ARG_CHECK(ops->ld >= n && ops->ld % 32 == 0, "ld must be >= n and a multiple of 32");
   SCSF_ARG_CHECK(ops->coef != nullptr, "coef is NULL");
+  SCSF_ARG_CHECK(ops->stencil == SCSF_STENCIL_FLUX || ops->stencil == SCSF_STENCIL_VIB13,
+                 "unknown stencil kind %d", ops->stencil);
+  SCSF_ARG_CHECK(ops->stencil == SCSF_STENCIL_FLUX || ops->dim == 2, "the 13-point vibration stencil is 2-D");
+  SCSF_ARG_CHECK(ops->stencil == SCSF_STENCIL_FLUX || (ops->nx >= 3 && ops->ny >= 3),
+                 "the 13-point vibration stencil needs nx, ny >= 3");
   return SCSF_OK;
 }
 
@@ -173,10 +180,27 @@ int scsf_assemble(const scsf_ops* ops, double h, const double* faces_x, const do
   scsf_ops o = *ops;
   o.coef = coef_out;
   SCSF_TRY(check_ops(&o));
+  SCSF_ARG_CHECK(ops->stencil == SCSF_STENCIL_FLUX, "scsf_assemble builds flux-form stencils (stencil = 0)");
   SCSF_ARG_CHECK(faces_x && faces_y && (ops->dim == 2 || faces_z), "face arrays missing");
   SCSF_ARG_CHECK(h > 0.0, "h must be > 0");
   cudaStream_t s = (cudaStream_t)stream;
   SCSF_TRY(assemble_impl(&o, h, faces_x, faces_y, faces_z, c, coef_out, s));
+  SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
+  return SCSF_OK;
+}
+
+int scsf_assemble_vibration(const scsf_ops* ops, double h, const double* D, const double* rho,
+                            int64_t field_stride, double* coef_out, void* stream) {
+  SCSF_ARG_CHECK(ops != nullptr, "ops is NULL");
+  scsf_ops o = *ops;
+  o.coef = coef_out;
+  SCSF_TRY(check_ops(&o));
+  SCSF_ARG_CHECK(o.stencil == SCSF_STENCIL_VIB13, "ops->stencil must be SCSF_STENCIL_VIB13");
+  SCSF_ARG_CHECK(D && rho, "D / rho NULL");
+  SCSF_ARG_CHECK(field_stride >= (int64_t)o.nx * o.ny, "field_stride must be >= n");
+  SCSF_ARG_CHECK(h > 0.0, "h must be > 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  SCSF_TRY(assemble_vib_impl(&o, h, D, rho, field_stride, coef_out, s));
   SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
   return SCSF_OK;
 }
@@ -193,10 +217,11 @@ int scsf_grf_fields(int32_t dim, int32_t nx, int32_t K, double s, double sigma, 
   SCSF_ARG_CHECK(nx >= 1 && n_ops >= 0, "nx >= 1 and n_ops >= 0 required");
   SCSF_ARG_CHECK(K >= 1 && (dim == 2 ? K <= 32 : K * K * K <= 1024), "K out of range (2-D: <= 32, 3-D: K^3 <= 1024)");
   SCSF_ARG_CHECK(dim == 2 || nx + 1 <= 64, "3-D fields need nx <= 63");
-  SCSF_ARG_CHECK(family >= 0 && family <= 2, "family must be 0 (diva), 1 (lapv) or 2 (divac)");
+  SCSF_ARG_CHECK(family >= 0 && family <= 3, "family must be 0 (diva), 1 (lapv), 2 (divac) or 3 (vib)");
   SCSF_ARG_CHECK(s >= 0.0 && vscale > 0.0, "s >= 0 and vscale > 0 required");
   if (n_ops == 0) return SCSF_OK;
-  SCSF_ARG_CHECK(xi && faces_x && faces_y && (dim == 2 || faces_z) && c && params, "NULL array");
+  SCSF_ARG_CHECK(xi && params && (family == 3 || (faces_x && faces_y && (dim == 2 || faces_z) && c)),
+                 "NULL array");
   if (!ws || ws_bytes < grf_ws_doubles(nx, K) * sizeof(double)) {
     set_error("workspace too small: need %zu bytes", grf_ws_doubles(nx, K) * sizeof(double));
     return SCSF_ERR_WORKSPACE;
@@ -701,6 +726,10 @@ void scsf_slab_rows(int32_t ny, int32_t world, int32_t rank, int32_t* y0, int32_
 
 static int check_dist(const scsf_ops* ops, int32_t y0, int32_t y1, const scsf_comm* comm) {
   SCSF_ARG_CHECK(comm != nullptr, "comm is NULL");
+  if (ops->stencil != SCSF_STENCIL_FLUX) {
+    set_error("the row-partitioned solve supports the flux-form stencil only");
+    return SCSF_ERR_NOT_IMPLEMENTED;
+  }
   SCSF_ARG_CHECK(ops->dim == 2, "the row-partitioned solve is 2-D (got dim %d)", ops->dim);
   SCSF_ARG_CHECK(ops->nx % 4 == 0, "the row-partitioned solve needs nx %% 4 == 0 (got %d)", ops->nx);
   SCSF_ARG_CHECK(0 <= y0 && y0 < y1 && y1 <= ops->ny, "slab rows [%d, %d) invalid for ny = %d", y0, y1, ops->ny);

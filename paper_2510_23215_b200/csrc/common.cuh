@@ -9,6 +9,9 @@
 
 namespace scsf {
 
+// coefficient arrays per operator (include/scsf.h stencil kinds)
+inline int ncoef(const scsf_ops* o) { return o->stencil == SCSF_STENCIL_VIB13 ? 7 : 1 + o->dim; }
+
 // ---------------------------------------------------------------- errors ----
 void set_error(const char* fmt, ...);
 void count_launch(int n = 1);

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(GRF_T) k_grf_eval(GrfArgs a) {
   }
   if (arr > dim || (dim == 2 ? y0 >= Hy : z >= Hz)) return;
   if (arr > 0 && f != 0) return;                   // only field 0 has face coefficients
-  const double scale = a.family == 2 ? 1.0 : a.vscale;
+  const double scale = a.family >= 2 ? 1.0 : a.vscale;
   if (arr > 0 && !faces_wanted) {                  // lapv: a = 1 on every face
     double* out = a.faces[ax] + (int64_t)op * plane_pts * Hz + (int64_t)z * plane_pts;
     for (int64_t p = (int64_t)y0 * Hx + threadIdx.x; p < (int64_t)y1 * Hx; p += GRF_T) out[p] = 1.0;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(GRF_T) k_grf_eval(GrfArgs a) {
     if (arr == 0) {
       a.params[((int64_t)op * a.n_fields + f) * n + idx] = v;
       if (a.family == 1 || (a.family == 2 && f == 1)) a.c[(int64_t)op * n + idx] = v;
-      else if (a.family == 0 || (a.family == 2 && a.n_fields == 1)) a.c[(int64_t)op * n + idx] = 0.0;
+      else if (a.family == 0) a.c[(int64_t)op * n + idx] = 0.0;
     } else {
       a.faces[ax][(int64_t)op * plane_pts * Hz + idx] = v;
     }
@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(GRF_T) k_grf_eval(GrfArgs a) {
 
 size_t grf_ws_doubles(int nx, int K) { return (size_t)2 * K * (nx + 1); }
 
-// family: 0 diva (-div(a grad u)), 1 lapv (-Lap u + V u), 2 divac (-div(a grad u) + c u)
+// family: 0 diva (-div(a grad u)), 1 lapv (-Lap u + V u), 2 divac (-div(a grad u) + c u),
+// 3 vib (thin plate: params = [D, rho] = [e^{g_0}, e^{g_1}], no faces / c)
 int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int family, int n_ops,
              const double* xi, double* fx, double* fy, double* fz, double* c, double* params, double* tab,
              cudaStream_t st) {
@@ -161,7 +162,7 @@ int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int 
   a.nx = nx;
   a.K = K;
   a.family = family;
-  a.n_fields = family == 2 ? 2 : 1;
+  a.n_fields = family >= 2 ? 2 : 1;
   a.n_ops = n_ops;
   a.s = s;
   a.sigma = sigma;
@@ -175,7 +176,7 @@ int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int 
   a.c = c;
   a.params = params;
   const int tiles = dim == 2 ? ceil_div(nx + 1, GRF_TY) : nx + 1;
-  dim3 g(tiles, 1 + dim, n_ops * a.n_fields);
+  dim3 g(tiles, family == 3 ? 1 : 1 + dim, n_ops * a.n_fields);   // vib: nodal fields only
   k_grf_eval<<<g, GRF_T, 0, st>>>(a);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;

@@ -585,11 +585,16 @@ __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restric
 
 // ----------------------------------------------------------------- lock ----
 // theta/res/wn/rel are indexed by block column (0..b-1); active columns [kL, b).
+constexpr double LOCK_FLOOR = 2.0;
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
                        const double* __restrict__ wn, double* __restrict__ rel, int b, int L,
                        double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg) {
   const int lane = threadIdx.x;            // one warp
   const int kL = ctrl->kL;
+  // Reading R26: the test ||r|| <= tol ||Av|| is capped at the fp64 floor of a computed
+  // residual, ||r|| <= LOCK_FLOOR eps beta (beta >= ||A||_2, Gershgorin).  It binds only when
+  // theta / beta < LOCK_FLOOR eps / tol (the vibration family: beta / theta_1 up to 1e8).
+  const double floor2 = (LOCK_FLOOR * 2.220446049250313e-16 * ctrl->beta) * (LOCK_FLOOR * 2.220446049250313e-16 * ctrl->beta);
   int first_bad = b, nonfin = 0;
   for (int base = kL; base < b; base += 32) {
     const int j = base + lane;
@@ -598,7 +603,7 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
       const double r = sqrt(res[j]) / sqrt(wn[j]);   // res, wn hold squared norms
       rel[j] = r;
       nonfin |= !isfinite(r);
-      bad = !(r <= tol);
+      bad = !(r <= tol || res[j] <= floor2);
     }
     const unsigned m = __ballot_sync(0xffffffffu, bad);
     if (m && first_bad == b) first_bad = base + __ffs(m) - 1;   // contiguous run from the bottom (R15)

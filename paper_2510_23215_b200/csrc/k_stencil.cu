@@ -147,6 +147,113 @@ __global__ void __launch_bounds__(ST_THREADS) k_stencil(
   }
 }
 
+// ------------------------------------------------ vibration (13-point) ----
+// Standard form of the thin-plate pencil (reading R25; include/scsf.h
+// SCSF_STENCIL_VIB13): B = S Lh diag(D) Lh S, S = diag(rho)^-1/2, Lh = (4 - neighbours)/h^2.
+// Entries of Lh diag(D) Lh written out per stencil offset (the sum over the shared
+// neighbours m of Lh(k,m) D_m Lh(m,l)):
+//   l = k        16 D_k + sum_{m in-grid x/y neighbour of k} D_m
+//   l = k+1      -4 (D_k + D_{k+1})           (same grid row)
+//   l = k+2      D_{k+1}                      (same grid row)
+//   l = k+nx-1   D_{k-1} + D_{k+nx}           (ix >= 1, iy < ny-1)
+//   l = k+nx     -4 (D_k + D_{k+nx})
+//   l = k+nx+1   D_{k+1} + D_{k+nx}           (ix < nx-1, iy < ny-1)
+//   l = k+2nx    D_{k+nx}
+// all / h^4, then times (rho_k rho_l)^-1/2.
+__global__ void k_assemble_vib(int nx, int ny, int64_t ld, double inv_h4, const double* __restrict__ D,
+                               const double* __restrict__ rho, int64_t fstride, double* __restrict__ coef) {
+  const int64_t n = (int64_t)nx * ny;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int op = blockIdx.y;
+  if (k >= ld) return;
+  double* out = coef + (int64_t)op * 7 * ld;
+  if (k >= n) {
+    for (int d = 0; d < 7; ++d) out[d * ld + k] = 0.0;
+    return;
+  }
+  const double* d = D + (int64_t)op * fstride;
+  const double* r = rho + (int64_t)op * fstride;
+  const int i = (int)(k % nx), j = (int)(k / nx);
+  const double sk = 1.0 / sqrt(r[k]);
+  auto s = [&](int64_t l) { return 1.0 / sqrt(r[l]); };
+  double dg = 16.0 * d[k];
+  if (i > 0) dg += d[k - 1];
+  if (i < nx - 1) dg += d[k + 1];
+  if (j > 0) dg += d[k - nx];
+  if (j < ny - 1) dg += d[k + nx];
+  out[k] = dg * inv_h4 * sk * sk;
+  out[ld + k] = (i < nx - 1) ? -4.0 * (d[k] + d[k + 1]) * inv_h4 * sk * s(k + 1) : 0.0;
+  out[2 * ld + k] = (i < nx - 2) ? d[k + 1] * inv_h4 * sk * s(k + 2) : 0.0;
+  out[3 * ld + k] = (i > 0 && j < ny - 1) ? (d[k - 1] + d[k + nx]) * inv_h4 * sk * s(k + nx - 1) : 0.0;
+  out[4 * ld + k] = (j < ny - 1) ? -4.0 * (d[k] + d[k + nx]) * inv_h4 * sk * s(k + nx) : 0.0;
+  out[5 * ld + k] = (i < nx - 1 && j < ny - 1) ? (d[k + 1] + d[k + nx]) * inv_h4 * sk * s(k + nx + 1) : 0.0;
+  out[6 * ld + k] = (j < ny - 2) ? d[k + nx] * inv_h4 * sk * s(k + 2 * nx) : 0.0;
+}
+
+// Gershgorin row sums of the 13-point stencil (upper arrays at k, lower ones at k - offset).
+__global__ void k_gershgorin_vib(const double* __restrict__ cf, int nx, int64_t n, int64_t ld,
+                                 unsigned long long* __restrict__ out) {
+  const int64_t off[6] = {1, 2, nx - 1, nx, nx + 1, 2 * (int64_t)nx};
+  double m = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double r = fabs(cf[k]);
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      r += fabs(cf[(a + 1) * ld + k]);
+      if (k >= off[a]) r += fabs(cf[(a + 1) * ld + k - off[a]]);
+    }
+    m = fmax(m, r);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// One filter step (or A X) with the 13-point stencil.  One point per thread, VB_COLS columns
+// per CTA sharing the 13 coefficient registers; the x-values of the 12 neighbours come through
+// L1/L2 (a column is nx*ny*8 B, re-read from cache by the neighbouring threads).  Zero
+// coefficients make the in-row wrap-arounds harmless; only the [0, n) range is guarded.
+constexpr int VB_THREADS = 256;
+constexpr int VB_COLS = 4;
+__global__ void __launch_bounds__(VB_THREADS) k_stencil_vib(
+    const double* __restrict__ cf, int64_t ldc, int nx, int64_t n, const double* __restrict__ X, const double* Xp,
+    double* Out, int64_t ldv, int ncols, const double* __restrict__ fp, int step) {
+  const int64_t k = (int64_t)blockIdx.x * VB_THREADS + threadIdx.x;
+  if (k >= ldv) return;
+  const int j0 = blockIdx.y * VB_COLS, j1 = min(ncols, j0 + VB_COLS);
+  if (k >= n) {                                        // ld padding stays 0
+    for (int j = j0; j < j1; ++j) Out[(int64_t)j * ldv + k] = 0.0;
+    return;
+  }
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int64_t o1 = 1, o2 = 2, o3 = nx - 1, o4 = nx, o5 = nx + 1, o6 = 2 * (int64_t)nx;
+  const double dg = cf[k] - c;
+  const double u1 = cf[ldc + k], u2 = cf[2 * ldc + k], u3 = cf[3 * ldc + k], u4 = cf[4 * ldc + k],
+               u5 = cf[5 * ldc + k], u6 = cf[6 * ldc + k];
+  const double l1 = k >= o1 ? cf[ldc + k - o1] : 0.0, l2 = k >= o2 ? cf[2 * ldc + k - o2] : 0.0;
+  const double l3 = k >= o3 ? cf[3 * ldc + k - o3] : 0.0, l4 = k >= o4 ? cf[4 * ldc + k - o4] : 0.0;
+  const double l5 = k >= o5 ? cf[5 * ldc + k - o5] : 0.0, l6 = k >= o6 ? cf[6 * ldc + k - o6] : 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double* __restrict__ x = X + (int64_t)j * ldv;
+    double v = dg * x[k];
+    if (k + o1 < n) v = fma(u1, x[k + o1], v);
+    if (k + o2 < n) v = fma(u2, x[k + o2], v);
+    if (k + o3 < n) v = fma(u3, x[k + o3], v);
+    if (k + o4 < n) v = fma(u4, x[k + o4], v);
+    if (k + o5 < n) v = fma(u5, x[k + o5], v);
+    if (k + o6 < n) v = fma(u6, x[k + o6], v);
+    if (k >= o1) v = fma(l1, x[k - o1], v);
+    if (k >= o2) v = fma(l2, x[k - o2], v);
+    if (k >= o3) v = fma(l3, x[k - o3], v);
+    if (k >= o4) v = fma(l4, x[k - o4], v);
+    if (k >= o5) v = fma(l5, x[k - o5], v);
+    if (k >= o6) v = fma(l6, x[k - o6], v);
+    v *= a;
+    if (b != 0.0) v = fma(b, Xp[(int64_t)j * ldv + k], v);
+    Out[(int64_t)j * ldv + k] = v;
+  }
+}
+
 // Vectorised variant: 4 consecutive points per thread, 256-bit loads/stores of
 // the column streams (Y_s, Y_{s-1}, Y_{s+1}) and the coefficient arrays;
 // x-neighbours k-1 / k+4 as scalars (same cache lines), y/z-neighbours as
@@ -645,7 +752,7 @@ int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, 
                       const double* fp, int step, cudaStream_t s) {
   if (ncols <= 0) return SCSF_OK;
   const int64_t n_glob = (int64_t)ops->nx * ops->ny;
-  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
   constexpr int CB = 2;
   dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
   k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
@@ -710,19 +817,30 @@ int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double*
   return SCSF_OK;
 }
 
+int assemble_vib_impl(const scsf_ops* ops, double h, const double* D, const double* rho, int64_t fstride,
+                      double* coef, cudaStream_t s) {
+  dim3 g(ceil_div(ops->ld, 256), ops->n_ops);
+  k_assemble_vib<<<g, 256, 0, s>>>(ops->nx, ops->ny, ops->ld, 1.0 / (h * h * h * h), D, rho, fstride, coef);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
+}
+
 int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s) {
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
-  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
   SCSF_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
   int blocks = min(ceil_div(n, 256), 148 * 4);
-  k_gershgorin<<<blocks, 256, 0, s>>>(cf, ops->dim, ops->nx, ops->ny, n, ops->ld, out);
+  if (ops->stencil == SCSF_STENCIL_VIB13)
+    k_gershgorin_vib<<<blocks, 256, 0, s>>>(cf, ops->nx, n, ops->ld, out);
+  else
+    k_gershgorin<<<blocks, 256, 0, s>>>(cf, ops->dim, ops->nx, ops->ny, n, ops->ld, out);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
 
 static int g_res_attr = 0;
 static int cluster_size_for(const scsf_ops* ops) {
-  if (ops->dim != 2 || ops->nx % 2 != 0) return 0;
+  if (ops->stencil != SCSF_STENCIL_FLUX || ops->dim != 2 || ops->nx % 2 != 0) return 0;
   for (int cs = 1; cs <= 8; cs *= 2) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024)
@@ -733,13 +851,14 @@ static int cluster_size_for(const scsf_ops* ops) {
 
 // 2: cluster-resident (k_filter_cl), 1: single-CTA resident (k_filter_res2d*), 0: per-step streaming
 int filter_kind(const scsf_ops* ops) {
+  if (ops->stencil != SCSF_STENCIL_FLUX) return 0;
   if (cluster_size_for(ops) > 0) return 2;
   if (ops->dim == 2 && (int64_t)ops->nx * ops->ny <= RES_MAX_N) return 1;
   return 0;
 }
 
 bool filter_resident_ok(const scsf_ops* ops) {
-  return cluster_size_for(ops) > 0 || (ops->dim == 2 && (int64_t)ops->nx * ops->ny <= RES_MAX_N);
+  return filter_kind(ops) > 0;
 }
 
 template <int CS, int CB>
@@ -790,7 +909,7 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
                          const double* fp, int m, cudaStream_t s, const int* deg) {
   if (ncols <= 0) return SCSF_OK;
   const int n = ops->nx * ops->ny;
-  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
   SCSF_TRY(stencil_init_attrs());
   const bool pair = (ops->nx % 2 == 0) && (ldv % 2 == 0) && (ops->ld % 2 == 0) && ((uintptr_t)X % 16 == 0) &&
                     ((uintptr_t)Out % 16 == 0) && ((uintptr_t)cf % 16 == 0);
@@ -824,7 +943,13 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
                  int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s) {
   if (ncols <= 0) return SCSF_OK;
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
-  const double* cf = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+  const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
+  if (ops->stencil == SCSF_STENCIL_VIB13) {
+    dim3 g(ceil_div(ldv, VB_THREADS), ceil_div(ncols, VB_COLS));
+    k_stencil_vib<<<g, VB_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n, X, Xp, Out, ldv, ncols, fp, step);
+    SCSF_LAUNCH_CHECK();
+    return SCSF_OK;
+  }
   const bool vec = (ops->nx % 4 == 0) && (ldv % 4 == 0) && (ops->ld % 4 == 0) &&
                    ((uintptr_t)X % 32 == 0) && ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0) &&
                    (Xp == nullptr || (uintptr_t)Xp % 32 == 0);

@@ -108,7 +108,7 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.perm = a.take<int>(b);
   w.ctrl = a.take<Ctrl>(1);
   w.gersh = a.take<unsigned long long>(1);
-  w.coef_buf = a.take<double>((int64_t)(1 + ops->dim) * ops->ld);
+  w.coef_buf = a.take<double>((int64_t)ncoef(ops) * ops->ld);
   w.deg = a.take<int>(b);
   if (dist && dist->comm) {
     const int64_t hb = (int64_t)b * ops->nx;
@@ -409,7 +409,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   scsf_ops opl = *ops_in;
   int op = op_in;
   if (graphs) {
-    const size_t per = (size_t)(1 + ops_in->dim) * ops_in->ld;
+    const size_t per = (size_t)ncoef(ops_in) * ops_in->ld;
     SCSF_CUDA_CHECK(cudaMemcpyAsync(w.coef_buf, ops_in->coef + (int64_t)op_in * per, per * sizeof(double),
                                     cudaMemcpyDeviceToDevice, s));
     opl.coef = w.coef_buf;
@@ -420,7 +420,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   int64_t spmm_cols = 0;
   int filter_steps = 0, iters = 0;
   double filter_bytes = 0.0;
-  const double coef_bytes = 8.0 * (1 + ops->dim) * (double)w.n;
+  const double coef_bytes = 8.0 * ncoef(ops) * (double)w.n;
   PhaseTimer tm;
   SCSF_TRY(tm.init());
   Ctrl h{};
@@ -487,7 +487,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     if (graphs && ba <= 128) {          // b > 128: the block Jacobi synchronises per sweep (not capturable)
       GraphKey key{};
       key.V = w.V;
-      key.coef = ops->coef + (int64_t)op * (1 + ops->dim) * ops->ld;
+      key.coef = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
       key.n = w.n;
       key.ldv = w.ldv;
       key.ld = ops->ld;

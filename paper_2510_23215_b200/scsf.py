@@ -31,6 +31,7 @@ EXPORTED = [
     "scsf_comm_rank", "scsf_slab_rows", "scsf_solve_dist_workspace_bytes", "scsf_solve_queue_dist",
     "scsf_filter_kind", "scsf_solve_chains_host_workspace_bytes", "scsf_solve_chains_host",
     "scsf_chain_state_doubles", "scsf_solve_chains_resume", "scsf_grf_workspace_bytes", "scsf_grf_fields",
+    "scsf_assemble_vibration",
 ]
 
 
@@ -46,7 +47,7 @@ class NotConverged(ScsfError):
 
 class scsf_ops(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
-                ("nz", ctypes.c_int32), ("n_ops", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("nz", ctypes.c_int32), ("n_ops", ctypes.c_int32), ("stencil", ctypes.c_int32),
                 ("ld", ctypes.c_int64), ("coef", ctypes.c_void_p)]
 
 
@@ -106,6 +107,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                   ST, P, SZ, P]),
         "scsf_chain_state_doubles": (I64, [OPS, I32, I32]),
         "scsf_grf_workspace_bytes": (SZ, [I32, I32]),
+        "scsf_assemble_vibration": (ctypes.c_int, [OPS, D, P, P, I64, P, P]),
         "scsf_grf_fields": (ctypes.c_int, [I32, I32, I32, D, D, D, I32, I32, P, P, P, P, P, P, P, SZ, P]),
         "scsf_solve_chains_resume": (ctypes.c_int, [OPS, P, P, I32, I32, I32, I32, D, I32, ctypes.c_uint64, P, P,
                                                     P, P, I64, ST, P, SZ, P]),
@@ -177,6 +179,9 @@ def ld_for(n: int) -> int:
 
 
 # ------------------------------------------------------------------ operators ----
+STENCIL_FLUX, STENCIL_VIB13 = 0, 1
+
+
 @dataclass
 class Operators:
     """A device batch of symmetric DIA stencils (include/scsf.h `scsf_ops`)."""
@@ -186,14 +191,16 @@ class Operators:
     nz: int
     n_ops: int
     ld: int
-    coef: torch.Tensor          # [n_ops, 1+dim, ld] float64 on the device
+    coef: torch.Tensor          # [n_ops, ncoef, ld] float64 on the device (ncoef = 1+dim, or 7 for VIB13)
+    stencil: int = 0            # STENCIL_FLUX or STENCIL_VIB13 (include/scsf.h)
 
     @property
     def n(self) -> int:
         return self.nx * self.ny * self.nz
 
     def c_struct(self) -> scsf_ops:
-        return scsf_ops(self.dim, self.nx, self.ny, self.nz, self.n_ops, 0, self.ld, self.coef.data_ptr())
+        return scsf_ops(self.dim, self.nx, self.ny, self.nz, self.n_ops, self.stencil, self.ld,
+                        self.coef.data_ptr())
 
 
 def assemble(dim: int, nx: int, h: float, faces, c: torch.Tensor | None) -> Operators:
@@ -216,7 +223,7 @@ def assemble(dim: int, nx: int, h: float, faces, c: torch.Tensor | None) -> Oper
     return ops
 
 
-GRF_FAMILIES = {"diva": 0, "lapv": 1, "divac": 2}
+GRF_FAMILIES = {"diva": 0, "lapv": 1, "divac": 2, "vib": 3}
 
 
 def grf_fields(dim: int, nx: int, K: int, s: float, sigma: float | None, vscale: float, family: str,
@@ -226,24 +233,45 @@ def grf_fields(dim: int, nx: int, K: int, s: float, sigma: float | None, vscale:
     lib = load_library()
     _require_cuda_f64(xi, "xi")
     fam = GRF_FAMILIES[family]
-    F = 2 if fam == 2 else 1
+    F = 2 if fam >= 2 else 1
     N = xi.shape[0]
     if xi.shape[1:] != (F, K ** dim):
         raise ValueError(f"xi must be [N, {F}, {K ** dim}]")
     n = nx ** dim
     dev = xi.device
     faces = []
-    for ax in range(dim):
+    for ax in range(dim if fam != 3 else 0):              # vib: nodal D, rho only
         shp = [nx] * dim
         shp[dim - 1 - ax] = nx + 1
         faces.append(torch.empty((N, *shp), dtype=torch.float64, device=dev))
-    c = torch.empty((N, n), dtype=torch.float64, device=dev)
+    c = torch.empty((N, n), dtype=torch.float64, device=dev) if fam != 3 else None
     params = torch.empty((N, F, n), dtype=torch.float64, device=dev)
     ws = _workspace(lib.scsf_grf_workspace_bytes(nx, K), dev)
+    fp = [_ptr(faces[ax]) if ax < len(faces) else None for ax in range(3)]
     _check(lib.scsf_grf_fields(dim, nx, K, s, -1.0 if sigma is None else sigma, vscale, fam, N, _ptr(xi),
-                               _ptr(faces[0]), _ptr(faces[1]), _ptr(faces[2]) if dim == 3 else None, _ptr(c),
+                               fp[0], fp[1], fp[2], _ptr(c),
                                _ptr(params), _ptr(ws), ws.numel(), _stream()))
     return faces, c, params
+
+
+def assemble_vibration(nx: int, h: float, params: torch.Tensor) -> Operators:
+    """Thin-plate vibration operators B = rho^-1/2 Lh D Lh rho^-1/2 on the device
+    (scsf_assemble_vibration).  params: cuda float64 [N, 2, n] with D = params[:, 0], rho = params[:, 1]."""
+    lib = load_library()
+    _require_cuda_f64(params, "params")
+    n = nx * nx
+    if params.dim() != 3 or params.shape[1] != 2 or params.shape[2] != n:
+        raise ValueError(f"params must be [N, 2, {n}]")
+    n_ops = params.shape[0]
+    ld = ld_for(n)
+    coef = torch.empty((n_ops, 7, ld), dtype=torch.float64, device=params.device)
+    ops = Operators(2, nx, nx, 1, n_ops, ld, coef, STENCIL_VIB13)
+    st = ops.c_struct()
+    D = params[:, 0]
+    rho = params[:, 1]
+    _check(lib.scsf_assemble_vibration(ctypes.byref(st), h, ctypes.c_void_p(D.data_ptr()),
+                                       ctypes.c_void_p(rho.data_ptr()), 2 * n, _ptr(coef), _stream()))
+    return ops
 
 
 # ----------------------------------------------------------------------- sort ----

@@ -68,9 +68,11 @@ CONFIGS = {
 
 # SURVEY §8(f) f3, beyond BASELINE.json's five configs: the paper's fourth dataset, thin-plate
 # vibration Lap(D Lap u) = lambda rho u, D and rho lognormal GRF fields
-# ("derived using GRF"), n = 10^4 as the paper's largest comparison.
+# ("derived using GRF"), n = 10^4 and L = 200, tol 1e-8 as the paper's smallest
+# vibration comparison (caption P:942).
 EXTRA_CONFIGS = {
-    "V1": Config("V1", 2, 100, 200, 50, "vib", K=8, s=1.0, sigma=0.3, chains=8),
+    # max_iter 500: a cold start needs 100-250 outer iterations on this spectrum (beta / lambda_L ~ 2e3)
+    "V1": Config("V1", 2, 100, 200, 200, "vib", K=8, s=1.0, sigma=0.3, max_iter=500, chains=8),
 }
 
 

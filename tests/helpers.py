@@ -8,6 +8,9 @@ from oracle import checks, eig as oeig, operator as oop
 def device_problem(fields, device="cuda"):
     import torch
     from paper_2510_23215_b200 import scsf
+    if getattr(fields, "is_vib", False):
+        params = torch.from_numpy(np.ascontiguousarray(fields.params)).to(device)
+        return scsf.assemble_vibration(fields.nx, fields.h, params), params
     faces = [torch.from_numpy(np.ascontiguousarray(f)).to(device) for f in fields.faces]
     c = torch.from_numpy(np.ascontiguousarray(fields.c)).to(device)
     params = torch.from_numpy(np.ascontiguousarray(fields.params)).to(device)

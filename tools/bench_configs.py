@@ -14,7 +14,7 @@ sys.path.insert(0, ".")
 import synth  # noqa: E402
 from paper_2510_23215_b200 import scsf  # noqa: E402
 
-PLAN = {"C1": (64, 8), "C2": (1000, 32), "C3": (64, 32), "C4": (64, 32), "C5": (8, 8)}
+PLAN = {"C1": (64, 8), "C2": (1000, 32), "C3": (64, 32), "C4": (64, 32), "C5": (8, 8), "V1": (200, 32)}
 
 
 def main():
@@ -25,9 +25,12 @@ def main():
         cfg = synth.get_config(name)
         N, C = PLAN[name]
         f = synth.make_batch(cfg, N)
-        faces = [torch.from_numpy(x).to(dev) for x in f.faces]
-        ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).to(dev))
         params = torch.from_numpy(f.params).to(dev)
+        if f.is_vib:
+            ops = scsf.assemble_vibration(cfg.nx, cfg.h, params)
+        else:
+            faces = [torch.from_numpy(x).to(dev) for x in f.faces]
+            ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).to(dev))
         perm, _, _ = scsf.sort(params, cfg.dim, cfg.nx, cfg.p0)
         scsf.solve_chains(ops, perm, C, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter,
                           seed=3, want_vecs=False, raise_on_fail=False)           # warm-up pass (graph cache)
