@@ -137,13 +137,17 @@ constexpr int V2_T = 64, V2_KC = 32, V2_P = V2_KC + 4;   // tile, k-chunk, pitch
 constexpr int V2_NT = 128;                                 // threads per CTA
 
 // ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
+// TN pipeline: k-chunks of 16 in a 4-stage cp.async ring (3 chunks in flight): the Gram products
+// stream X and Y once with little reuse per CTA, so load latency, not DMMA, bounds a short chunk loop.
+constexpr int TN_KC = 16, TN_P = TN_KC + 4, TN_ST = 4;
+
 __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
                                                   const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
                                                   int64_t kchunk, int upper, int a16, double* __restrict__ P,
                                                   const double* __restrict__ Y2) {
   extern __shared__ __align__(16) double smd[];
-  double* xs = smd;                                  // [2][64][36]
-  double* ys = smd + 2 * V2_T * V2_P;                // [2][64][36]
+  double* xs = smd;                                  // [TN_ST][64][20]
+  double* ys = smd + TN_ST * V2_T * TN_P;            // [TN_ST][64][20]
   // dual mode (Y2 != NULL): output columns [0, b2) = X^T Y (upper rule), [b2, 2 b2) = X^T Y2 (full)
   const int T2 = (b2 + V2_T - 1) / V2_T;
   const int grp = Y2 ? (int)blockIdx.y / T2 : 0;
@@ -158,18 +162,18 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const int nck = (int)((kend - kbeg + V2_KC - 1) / V2_KC);
+  const int nck = (int)((kend - kbeg + TN_KC - 1) / TN_KC);
 
   auto issue = [&](int c, int stage) {
-    const int64_t k0 = kbeg + (int64_t)c * V2_KC;
+    const int64_t k0 = kbeg + (int64_t)c * TN_KC;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = tid + V2_NT * q;             // 0..1023
-      const int col = idx >> 4, seg = idx & 15;    // 64 columns x 16 16-byte segments
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + V2_NT * q;             // 0..511
+      const int col = idx >> 3, seg = idx & 7;     // 64 columns x 8 16-byte segments
       const int64_t k = k0 + 2 * seg;
       const int rem = (int)max((int64_t)0, min((int64_t)2, kend - k));
-      double* dx = xs + (stage * V2_T + col) * V2_P + 2 * seg;
-      double* dy = ys + (stage * V2_T + col) * V2_P + 2 * seg;
+      double* dx = xs + (stage * V2_T + col) * TN_P + 2 * seg;
+      double* dy = ys + (stage * V2_T + col) * TN_P + 2 * seg;
       const bool okx = (i0 + col < b1) && rem > 0, oky = (j0 + col < b2) && rem > 0;
       const double* sx = okx ? X + k + (int64_t)(i0 + col) * ldx : X;
       const double* sy = oky ? Y + k + (int64_t)(j0 + col) * ldy : Y;
@@ -191,32 +195,31 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  issue(0, 0);
-  cp_commit();
-  for (int c = 0; c < nck; ++c) {
-    if (c + 1 < nck) {
-      issue(c + 1, (c + 1) & 1);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const double* xa = xs + ((c & 1) * V2_T + wm + g) * V2_P + t;
-    const double* yb = ys + ((c & 1) * V2_T + wn + g) * V2_P + t;
 #pragma unroll
-    for (int kk = 0; kk < V2_KC; kk += 4) {
+  for (int st = 0; st < TN_ST - 1; ++st) {
+    if (st < nck) issue(st, st);
+    cp_commit();
+  }
+  for (int c = 0; c < nck; ++c) {
+    cp_wait<TN_ST - 2>();                            // chunk c has landed (this thread's copies) ...
+    __syncthreads();                                 // ... everyone's, and chunk c-1's stage is free
+    if (c + TN_ST - 1 < nck) issue(c + TN_ST - 1, (c + TN_ST - 1) % TN_ST);
+    cp_commit();
+    const int stage = c % TN_ST;
+    const double* xa = xs + (stage * V2_T + wm + g) * TN_P + t;
+    const double* yb = ys + (stage * V2_T + wn + g) * TN_P + t;
+#pragma unroll
+    for (int kk = 0; kk < TN_KC; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * V2_P + kk];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * TN_P + kk];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = yb[ni * 8 * V2_P + kk];
+      for (int ni = 0; ni < 4; ++ni) b[ni] = yb[ni * 8 * TN_P + kk];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
     }
-    __syncthreads();
   }
   double* out = P + (int64_t)blockIdx.z * b1 * b2tot;
 #pragma unroll
@@ -361,7 +364,7 @@ int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s) {
 // ------------------------------------------------------------------ host ----
 static int g_nn_smem_set = 0;
 
-static size_t tn2_smem() { return (size_t)4 * V2_T * V2_P * sizeof(double); }
+static size_t tn2_smem() { return (size_t)2 * TN_ST * V2_T * TN_P * sizeof(double); }
 static size_t nn2_smem(int b1) {
   const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
   return ((size_t)b1r * (V2_T + 4) + (size_t)2 * V2_T * V2_P) * sizeof(double);
@@ -420,7 +423,7 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
     const int t = ceil_div(b1, V2_T);
     splits = min(max(1, ceil_div(n, tn_min_rows())), max(1, (2 * 148 + t * (t + 1) / 2 - 1) / (t * (t + 1) / 2)));
   }
-  int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
+  int64_t kchunk = round_up(ceil_div(n, splits), TN_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
   const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
@@ -442,7 +445,7 @@ int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y
   const int t = ceil_div(b, V2_T);
   const int tiles = t * (t + 1);
   int splits = min(max(1, ceil_div(n, tn_min_rows())), max(1, (2 * 148 + tiles - 1) / tiles));
-  int64_t kchunk = round_up(ceil_div(n, splits), V2_KC);
+  int64_t kchunk = round_up(ceil_div(n, splits), TN_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(t, 2 * t, splits);
   const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
