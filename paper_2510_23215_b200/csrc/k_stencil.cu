@@ -672,6 +672,174 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_filter_rp: the cluster-resident filter with register-resident 2 x 4 patches.  Same
+// slab / ghost-row / DSMEM layout as k_filter_cl, but a thread keeps its patch of Y_s and
+// Y_{s-1} (4 rows x 2 points) in registers for all m steps, so per step it reads only the
+// rows just below and above its patch from shared memory (plus x-neighbours across warp
+// edges) and stores its new rows for the neighbours: 2 loads + 4 stores + 8 shuffles per
+// 8 points against 6 loads + 2 stores + 4 shuffles per 4 points in k_filter_cl (ncu: that
+// kernel stalls on the shared-memory instruction queue, mio_throttle; this one halves the
+// shared wavefronts, but at 168 registers a 352-thread CTA fills the register file, so it
+// only wins where k_filter_cl has few threads per column: see cluster_size_rp).
+constexpr int RP_T = 384;                        // max threads (patches) per CTA (<= 170 registers)
+constexpr int RP_ROWS = 4;
+
+template <int CS, int CB>
+__global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
+                                                       const double* __restrict__ X, int64_t ldv, int ncols,
+                                                       double* __restrict__ Out, const double* __restrict__ fp, int m,
+                                                       const int* __restrict__ deg) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
+  __shared__ double sa[128], sb[128];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+  const int R = ((ny + CS - 1) / CS + RP_ROWS - 1) / RP_ROWS * RP_ROWS;
+  const int row0 = rank * R;
+  const int rows = max(0, min(R, ny - row0));
+  const int hx = nx >> 1;
+  const int npatch = ((rows + RP_ROWS - 1) / RP_ROWS) * hx;
+  const int pitch = (R + 2) * nx;
+  const int n = nx * ny;
+  const int ncb = min(CB, ncols - j0);
+  int mcol[CB];
+  int mrun = 0;
+#pragma unroll
+  for (int cc = 0; cc < CB; ++cc) {
+    mcol[cc] = (cc < ncb) ? (deg ? max(1, min(m, deg[j0 + cc])) : m) : 0;
+    mrun = max(mrun, mcol[cc]);
+  }
+  const double c = fp[1];
+  if (tid == 0) {                                          // Alg. 1 scalars, as step_scalars()
+    const double lam = fp[0], e = fp[2];
+    const double s1 = e / (lam - c);
+    double sig = s1;
+    sa[0] = s1 / e;
+    sb[0] = 0.0;
+    for (int st = 1; st < m && st < 128; ++st) {
+      const double sn = 1.0 / (2.0 / s1 - sig);
+      sa[st] = 2.0 * sn / e;
+      sb[st] = -sn * sig;
+      sig = sn;
+    }
+  }
+  const bool has_lo = rank > 0;
+  const bool has_hi = (rank + 1 < CS) && (row0 + R < ny);
+  double* lo_buf = has_lo ? cluster.map_shared_rank(cbuf, rank - 1) : nullptr;
+  double* hi_buf = has_hi ? cluster.map_shared_rank(cbuf, rank + 1) : nullptr;
+  for (int i = tid; i < CB * pitch; i += nthr) sts2(cbuf + 2 * i, make_double2(0.0, 0.0));
+  cluster_barrier();
+  for (int cc = 0; cc < ncb; ++cc) {                       // Y_0 into buffer 0 (own rows + neighbours' ghosts)
+    const double* x0 = X + (int64_t)(j0 + cc) * ldv + (int64_t)row0 * nx;
+    double* b0 = cbuf + (size_t)(2 * cc) * pitch;
+    for (int q = tid; q < rows * hx; q += nthr) {
+      const double2 v = *reinterpret_cast<const double2*>(x0 + 2 * q);
+      sts2(b0 + nx + 2 * q, v);
+      const int lr = q / hx, xq = 2 * (q % hx);
+      if (lr == 0 && lo_buf) sts2(lo_buf + (size_t)(2 * cc) * pitch + (R + 1) * nx + xq, v);
+      if (lr == rows - 1 && hi_buf) sts2(hi_buf + (size_t)(2 * cc) * pitch + xq, v);
+    }
+  }
+  const bool act = tid < npatch;
+  const int pt = min(tid, max(npatch - 1, 0));
+  const int lr0 = RP_ROWS * (pt / hx), xq = 2 * (pt % hx);
+  const int nr = act ? min(RP_ROWS, rows - lr0) : 0;       // valid rows of this patch
+  const int g0 = (row0 + lr0) * nx + xq;
+  const double2 z2 = make_double2(0, 0);
+  double2 dg[RP_ROWS], cxp[RP_ROWS], cyp[RP_ROWS];
+  double cxm[RP_ROWS];
+  double2 cym0 = z2;
+#pragma unroll
+  for (int r = 0; r < RP_ROWS; ++r) {
+    dg[r] = z2; cxp[r] = z2; cyp[r] = z2; cxm[r] = 0.0;
+    if (npatch > 0 && lr0 + r < rows) {
+      const int g = g0 + r * nx;
+      dg[r] = *reinterpret_cast<const double2*>(cf + g);
+      dg[r].x -= c; dg[r].y -= c;
+      cxp[r] = *reinterpret_cast<const double2*>(cf + ldc + g);
+      cxm[r] = (g >= 1) ? __ldg(cf + ldc + g - 1) : 0.0;
+      cyp[r] = *reinterpret_cast<const double2*>(cf + 2 * ldc + g);
+    }
+  }
+  if (npatch > 0 && g0 >= nx) cym0 = *reinterpret_cast<const double2*>(cf + 2 * ldc + g0 - nx);
+  const bool fix_l = (lane == 0) || (xq == 0);
+  const bool fix_r = (lane == 31) || (xq + 2 == nx) || (tid + 1 >= npatch);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(cbuf);
+  const int l0 = (lr0 + 1) * nx + xq;                      // buffer index of the patch's row 0
+  const unsigned nx8 = 8u * nx;
+  unsigned acur[CB], anxt[CB];
+  double2 cur[CB][RP_ROWS], prv[CB][RP_ROWS];
+#pragma unroll
+  for (int cc = 0; cc < CB; ++cc) {
+    acur[cc] = sbase + 8u * (unsigned)((2 * cc) * pitch + l0);
+    anxt[cc] = sbase + 8u * (unsigned)((2 * cc + 1) * pitch + l0);
+#pragma unroll
+    for (int r = 0; r < RP_ROWS; ++r) {
+      prv[cc][r] = z2;
+      cur[cc][r] = (cc < ncb && r < nr)
+                       ? *reinterpret_cast<const double2*>(X + (int64_t)(j0 + cc) * ldv + g0 + r * nx) : z2;
+    }
+  }
+  const unsigned lo32 = has_lo ? mapa32(sbase, rank - 1) : 0u, hi32 = has_hi ? mapa32(sbase, rank + 1) : 0u;
+  const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;               // my row 0 -> row R + 1 below
+  const unsigned dhi = hi32 - sbase - (unsigned)rows * nx8;            // my top slab row -> row 0 above
+  const bool push_lo = act && has_lo && lr0 == 0;
+  const int rtop = (act && has_hi) ? rows - 1 - lr0 : -1;              // patch row that is the slab's top row
+  cluster_barrier();                                       // neighbours' ghosts of Y_0, sa / sb
+  for (int st = 0; st < mrun; ++st) {
+    const double a = sa[st], bco = sb[st];
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+      if (st < mcol[cc]) {                                 // uniform across the CTA
+        const unsigned ca = acur[cc], na = anxt[cc];
+        const double2 xd = lds2a(ca - nx8);                // row below the patch (ghost / other patch)
+        const double2 xu = lds2a(ca + RP_ROWS * nx8);      // row above the patch
+        double2 nw[RP_ROWS];
+#pragma unroll
+        for (int r = 0; r < RP_ROWS; ++r) {
+          const double2 xc = cur[cc][r];
+          double xl = __shfl_up_sync(0xffffffffu, xc.y, 1), xr = __shfl_down_sync(0xffffffffu, xc.x, 1);
+          if (fix_l) xl = lds1a(ca + r * nx8 - 8u);
+          if (fix_r) xr = lds1a(ca + r * nx8 + 16u);
+          const double2 bl = (r == 0) ? xd : cur[cc][r - 1];
+          const double2 ab = (r == RP_ROWS - 1) ? xu : cur[cc][r + 1];
+          const double2 cb = (r == 0) ? cym0 : cyp[r - 1];
+          double2 v;
+          v.x = fma(dg[r].x, xc.x, fma(cxp[r].x, xc.y, fma(cxm[r], xl, fma(cyp[r].x, ab.x, cb.x * bl.x))));
+          v.y = fma(dg[r].y, xc.y, fma(cxp[r].y, xr, fma(cxp[r].x, xc.x, fma(cyp[r].y, ab.y, cb.y * bl.y))));
+          v.x = fma(bco, prv[cc][r].x, a * v.x);
+          v.y = fma(bco, prv[cc][r].y, a * v.y);
+          nw[r] = (r < nr) ? v : z2;                       // rows past the slab stay 0 (Dirichlet)
+        }
+#pragma unroll
+        for (int r = 0; r < RP_ROWS; ++r) {
+          prv[cc][r] = cur[cc][r];
+          cur[cc][r] = nw[r];
+          if (r < nr) sts2a(na + r * nx8, nw[r]);
+          if (r == rtop) stc2a(na + r * nx8 + dhi, nw[r]);
+        }
+        if (push_lo) stc2a(na + dlo, nw[0]);
+        acur[cc] = na;
+        anxt[cc] = ca;
+      }
+    }
+    cluster_barrier();                                     // new rows and pushed ghosts complete cluster-wide
+  }
+#pragma unroll
+  for (int cc = 0; cc < CB; ++cc) {
+    if (cc < ncb) {
+      double* out = Out + (int64_t)(j0 + cc) * ldv;
+#pragma unroll
+      for (int r = 0; r < RP_ROWS; ++r)
+        if (r < nr) *reinterpret_cast<double2*>(out + g0 + r * nx) = cur[cc][r];
+      if (rank == CS - 1)
+        for (int k = n + tid; k < (int)ldv; k += nthr) out[k] = 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------ row-partitioned (slab) ----
 // Row partition of a 2-D operator: this rank owns grid rows
 // [y0, y1); vectors hold only those n_loc = nx (y1 - y0) rows, the operator
@@ -849,9 +1017,33 @@ static int cluster_size_for(const scsf_ops* ops) {
   return 0;
 }
 
-// 2: cluster-resident (k_filter_cl), 1: single-CTA resident (k_filter_res2d*), 0: per-step streaming
+// k_filter_rp: 2 x 4 register patches; SCSF_FILTER_RP=0 falls back to k_filter_cl
+static bool rp_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_FILTER_RP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+static int rp_rows(int ny, int cs) { return ((ny + cs - 1) / cs + RP_ROWS - 1) / RP_ROWS * RP_ROWS; }
+constexpr int RP_CB = 2;
+static int cluster_size_rp(const scsf_ops* ops) {
+  if (!rp_enabled() || ops->stencil != SCSF_STENCIL_FLUX || ops->dim != 2 || ops->nx % 2 != 0) return 0;
+  // Measured (tools/bench_configs.py): ahead of k_filter_cl when one CTA holds a whole column
+  // (C1, 32 x 32: 1150-1200 against 1010-1060 operators/s); on C2 (4-CTA clusters) k_filter_cl
+  // with 4 columns per CTA is as fast or faster (1400 against 1350), so only cs == 1 is used.
+  const int R = rp_rows(ops->ny, 1);
+  if ((R / RP_ROWS) * (ops->nx / 2) <= RP_T && (size_t)RP_CB * 2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024)
+    return 1;
+  return 0;
+}
+
+// 3: register-patch cluster filter (k_filter_rp), 2: cluster-resident (k_filter_cl),
+// 1: single-CTA resident (k_filter_res2d*), 0: per-step streaming
 int filter_kind(const scsf_ops* ops) {
   if (ops->stencil != SCSF_STENCIL_FLUX) return 0;
+  if (cluster_size_rp(ops) > 0) return 3;
   if (cluster_size_for(ops) > 0) return 2;
   if (ops->dim == 2 && (int64_t)ops->nx * ops->ny <= RES_MAX_N) return 1;
   return 0;
@@ -873,6 +1065,16 @@ static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* c
   if (cb == 4) return launch_cl1<CS, 4>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   if (cb == 2) return launch_cl1<CS, 2>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   return launch_cl1<CS, 1>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+}
+static cudaError_t launch_rp(cudaLaunchConfig_t& cfg, int cs, const double* cf, int64_t ldc, int nx, int ny,
+                             const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m,
+                             const int* deg) {
+  switch (cs) {
+    case 1: return cudaLaunchKernelEx(&cfg, k_filter_rp<1, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    case 2: return cudaLaunchKernelEx(&cfg, k_filter_rp<2, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    case 4: return cudaLaunchKernelEx(&cfg, k_filter_rp<4, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    default: return cudaLaunchKernelEx(&cfg, k_filter_rp<8, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  }
 }
 static cudaError_t launch_cl(cudaLaunchConfig_t& cfg, int cs, int cb, const double* cf, int64_t ldc, int nx, int ny,
                              const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m,
@@ -899,6 +1101,10 @@ int stencil_init_attrs() {
   SCSF_CL_ATTR(4, 1); SCSF_CL_ATTR(4, 2); SCSF_CL_ATTR(4, 4);
   SCSF_CL_ATTR(8, 1); SCSF_CL_ATTR(8, 2); SCSF_CL_ATTR(8, 4);
 #undef SCSF_CL_ATTR
+#define SCSF_RP_ATTR(CS) \
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_rp<CS, RP_CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+  SCSF_RP_ATTR(1); SCSF_RP_ATTR(2); SCSF_RP_ATTR(4); SCSF_RP_ATTR(8);
+#undef SCSF_RP_ATTR
   g_res_attr = 1;
   done = true;
   return SCSF_OK;
@@ -913,8 +1119,26 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
   SCSF_TRY(stencil_init_attrs());
   const bool pair = (ops->nx % 2 == 0) && (ldv % 2 == 0) && (ops->ld % 2 == 0) && ((uintptr_t)X % 16 == 0) &&
                     ((uintptr_t)Out % 16 == 0) && ((uintptr_t)cf % 16 == 0);
+  const int csr = pair ? cluster_size_rp(ops) : 0;
   const int cs = pair ? cluster_size_for(ops) : 0;
-  if (cs > 0) {
+  if (csr > 0) {
+    const int R = rp_rows(ops->ny, csr);
+    const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
+    const int thr = (int)round_up((int64_t)(R / RP_ROWS) * (ops->nx / 2), 32);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csr, ceil_div(ncols, RP_CB), 1);
+    cfg.blockDim = dim3(thr, 1, 1);
+    cfg.dynamicSmemBytes = per_col * RP_CB;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csr;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SCSF_CUDA_CHECK(launch_rp(cfg, csr, cf, ops->ld, ops->nx, ops->ny, X, ldv, ncols, Out, fp, m, deg));
+  } else if (cs > 0) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
     const int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);

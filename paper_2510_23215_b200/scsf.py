@@ -159,7 +159,8 @@ def launch_count() -> int:
     return int(load_library().scsf_launch_count())
 
 
-FILTER_KERNELS = {2: "k_filter_cl (cluster-resident whole filter, Alg. 1)",
+FILTER_KERNELS = {3: "k_filter_rp (cluster-resident whole filter, register patches, Alg. 1)",
+                  2: "k_filter_cl (cluster-resident whole filter, Alg. 1)",
                   1: "k_filter_res2d (single-CTA resident whole filter, Alg. 1)",
                   0: "k_stencil_v4 (one streaming launch per filter step, Alg. 1)"}
 
