@@ -44,7 +44,9 @@ def main():
         ms = e0.elapsed_time(e1)
         its = [s["iterations"] for s in st]
         out[name] = {"operators": N, "chains": C, "n": cfg.n, "L": cfg.L, "b": cfg.b,
-                     "filter_kernel": scsf.FILTER_KERNELS[scsf.filter_kind(ops)],
+                     "filter_kernel": ("k_stencil_vib (13-point streaming launch per filter step, Alg. 1)"
+                                       if ops.stencil == scsf.STENCIL_VIB13 else
+                                       scsf.FILTER_KERNELS[scsf.filter_kind(ops)]),
                      "operators_per_s": N / (ms / 1e3), "ms": ms,
                      "converged": int(sum(s["status"] == 0 for s in st)),
                      "iterations_mean": float(np.mean(its)), "iterations_max": int(max(its))}
