@@ -404,6 +404,19 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
   }
   __syncthreads();
   const double gfloor = floor_s;
+  // slot pairs (I <= J) of this thread: flat index k = tid + 1024 q over the upper triangle
+  constexpr int NBLK = H2 * (H2 + 1) / 2, JB_PER = (NBLK + 1023) / 1024;
+  int bI[JB_PER], bJ[JB_PER];
+#pragma unroll
+  for (int q = 0; q < JB_PER; ++q) {
+    int k = q * 1024 + tid, I = 0;
+    while (I < H2 && k >= H2 - I) {                 // row I holds slots J = I .. H2-1
+      k -= H2 - I;
+      ++I;
+    }
+    bI[q] = min(I, H2 - 1);
+    bJ[q] = min(I + k, H2 - 1);
+  }
   int nrec = 0;                                     // uniform across the CTA
   int sweep = 0;
   for (; sweep <= max_sweeps; ++sweep) {
@@ -453,37 +466,36 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
       if (!any_rot[par]) continue;                  // uniform: the record slot is reused
       if (tid == 0) recm[nrec] = m;
       ++nrec;
-      // ---- G <- J^T G J on blocks {ilo, ihi} x {jlo, jhi}, ilo <= jlo (upper storage)
-      for (int ai = warp; ai < H2; ai += 32) {
-        const int ilo = ins0(ai, h);
-        const int ihi = ilo ^ m;
-        const double2 cs1 = cs_cs[ilo];
-        for (int aj = ai + lane; aj < H2; aj += 32) {
-          const int jlo = ins0(aj, h);
-          const double2 cs2 = cs_cs[jlo];
-          if (cs1.y == 0.0 && cs2.y == 0.0) continue;
-          const int jhi = jlo ^ m;
-          if (ilo == jlo) {
-            const int ipq = ilo * GP + ihi;
-            const double gpq = G[ipq], t = cs_t[ilo];
-            G[ilo * GP + ilo] -= t * gpq;
-            G[ihi * GP + ihi] += t * gpq;
-            G[ipq] = 0.0;
-            continue;
-          }
-          const int ia = ilo * GP + jlo;
-          const int ib = ilo * GP + jhi;
-          const int ic = min(ihi, jlo) * GP + max(ihi, jlo);
-          const int id = min(ihi, jhi) * GP + max(ihi, jhi);
-          const double a = G[ia], bb = G[ib], cc = G[ic], d = G[id];
-          const double c1 = cs1.x, s1 = cs1.y, c2 = cs2.x, s2 = cs2.y;
-          const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;
-          const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
-          G[ia] = c1 * a2 - s1 * c2v;
-          G[ib] = c1 * b2 - s1 * d2;
-          G[ic] = s1 * a2 + c1 * c2v;
-          G[id] = s1 * b2 + c1 * d2;
+      // ---- G <- J^T G J on blocks {ilo, ihi} x {jlo, jhi}, ilo <= jlo (upper storage).  The
+      // H2 (H2 + 1) / 2 slot pairs (I <= J) are dealt to the threads once per launch (bI / bJ),
+      // so a round costs a few index operations per block and no idle lanes.
+#pragma unroll
+      for (int q = 0; q < JB_PER; ++q) {
+        if (q * 1024 + tid >= NBLK) break;
+        const int ilo = ins0(bI[q], h), jlo = ins0(bJ[q], h);
+        const double2 cs1 = cs_cs[ilo], cs2 = cs_cs[jlo];
+        if (cs1.y == 0.0 && cs2.y == 0.0) continue;
+        const int ihi = ilo ^ m, jhi = jlo ^ m;
+        if (ilo == jlo) {
+          const int ipq = ilo * GP + ihi;
+          const double gpq = G[ipq], t = cs_t[ilo];
+          G[ilo * GP + ilo] -= t * gpq;
+          G[ihi * GP + ihi] += t * gpq;
+          G[ipq] = 0.0;
+          continue;
         }
+        const int ia = ilo * GP + jlo;
+        const int ib = ilo * GP + jhi;
+        const int ic = min(ihi, jlo) * GP + max(ihi, jlo);
+        const int id = min(ihi, jhi) * GP + max(ihi, jhi);
+        const double a = G[ia], bb = G[ib], cc = G[ic], d = G[id];
+        const double c1 = cs1.x, s1 = cs1.y, c2 = cs2.x, s2 = cs2.y;
+        const double a2 = c2 * a - s2 * bb, b2 = s2 * a + c2 * bb;
+        const double c2v = c2 * cc - s2 * d, d2 = s2 * cc + c2 * d;
+        G[ia] = c1 * a2 - s1 * c2v;
+        G[ib] = c1 * b2 - s1 * d2;
+        G[ic] = s1 * a2 + c1 * c2v;
+        G[id] = s1 * b2 + c1 * d2;
       }
       __syncthreads();
     }
