@@ -349,6 +349,131 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_nn2(const double* __restrict__ X
   }
 }
 
+// ---- NN, wide tile: Out[r0:r0+64, j0:j0+128] per pass with 8 warps (2 x 4 warp grid of 32 x 32).
+// For large b (C3-C5, V1: b = 240-360) k_gemm_nn2's 176-KB panel leaves one 4-warp CTA per SM
+// and sweeps the panel b/64 times; here 8 warps share the panel and it is swept b/128 times.
+constexpr int NN3_T = 256, NN3_BN = 128;
+
+__global__ void __launch_bounds__(NN3_T) k_gemm_nn3(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
+                                                  const double* __restrict__ M, int64_t ldm, int b2,
+                                                  double alpha, double beta, double* Out, int64_t ldo,
+                                                  int tri_upper, int a16, int m16) {
+  extern __shared__ __align__(16) double smd[];
+  const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
+  double* xp = smd;                                  // [b1r][68]: xp[k*68 + r]
+  double* ms = smd + b1r * (V2_T + 4);               // [2][128][36]: ms[(st*128 + j)*36 + kk]
+  const int64_t r0 = (int64_t)blockIdx.x * V2_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;
+  const int nck_all = b1r / V2_KC;
+  const int rows_here = (int)min((int64_t)V2_T, n - r0);
+
+  auto issue_panel = [&](int c) {      // 32 k-columns x 64 rows: 1024 16-byte segments
+#pragma unroll
+    for (int q = 0; q < 1024 / NN3_T; ++q) {
+      const int idx = tid + NN3_T * q;
+      const int kk = idx >> 5, seg = idx & 31;
+      const int k = c * V2_KC + kk;
+      const int rr = 2 * seg;
+      const int rem = (k < b1) ? max(0, min(2, rows_here - rr)) : 0;
+      const double* src = rem ? X + r0 + rr + (int64_t)k * ldx : X;
+      double* dst = xp + k * (V2_T + 4) + rr;
+      if (a16) {
+        cp_async16(dst, src, 8 * rem);
+      } else {
+        cp_async8(dst, src, rem ? 8 : 0);
+        cp_async8(dst + 1, rem > 1 ? src + 1 : src, rem > 1 ? 8 : 0);
+      }
+    }
+  };
+  auto issue_m = [&](int c, int j0, int stage) {   // 128 columns x 32 k
+    if (m16) {
+#pragma unroll
+      for (int q = 0; q < 2048 / NN3_T; ++q) {
+        const int idx = tid + NN3_T * q;           // 0..2047
+        const int j = idx >> 4, seg = idx & 15;
+        const int k = c * V2_KC + 2 * seg;
+        const int rem = (j0 + j < b2) ? max(0, min(2, b1 - k)) : 0;
+        cp_async16(ms + (stage * NN3_BN + j) * V2_P + 2 * seg,
+                   rem ? (const void*)(M + k + (int64_t)(j0 + j) * ldm) : (const void*)M, 8 * rem);
+      }
+    } else {
+#pragma unroll 4
+      for (int q = 0; q < 4096 / NN3_T; ++q) {
+        const int idx = tid + NN3_T * q;           // 0..4095
+        const int j = idx >> 5, kk = idx & 31;
+        const int k = c * V2_KC + kk;
+        const bool ok = (k < b1) && (j0 + j < b2);
+        cp_async8(ms + (stage * NN3_BN + j) * V2_P + kk,
+                  ok ? (const void*)(M + k + (int64_t)(j0 + j) * ldm) : (const void*)M, ok ? 8 : 0);
+      }
+    }
+  };
+
+  for (int j0 = 0; j0 < b2; j0 += NN3_BN) {
+    const bool first = (j0 == 0);
+    const int nck = tri_upper ? min(nck_all, (min(b2, j0 + NN3_BN) + V2_KC - 1) / V2_KC) : nck_all;
+    const int ncp = first ? nck_all : 0;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int c = 0; c < 2 && c < nck; ++c) {
+      issue_m(c, j0, c);
+      if (c < ncp) issue_panel(c);
+      cp_commit();
+    }
+    for (int c = 0; c < nck; ++c) {
+      if (c + 1 < nck) cp_wait<1>();
+      else cp_wait<0>();
+      __syncthreads();
+      const double* xa = xp + (c * V2_KC + t) * (V2_T + 4) + wm + g;
+      const double* mb = ms + ((c & 1) * NN3_BN + wn + g) * V2_P + t;
+#pragma unroll
+      for (int kk = 0; kk < V2_KC; kk += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * (V2_T + 4) + mi * 8];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = mb[ni * 8 * V2_P + kk];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+      }
+      __syncthreads();
+      if (c + 2 < nck) {
+        issue_m(c + 2, j0, c & 1);
+        if (c + 2 < ncp) issue_panel(c + 2);
+        cp_commit();
+      }
+    }
+    if (first && nck < ncp) {
+      for (int c = nck; c < ncp; ++c) issue_panel(c);
+      cp_commit();
+      cp_wait<0>();
+    }
+    __syncthreads();                 // every warp is past its panel reads before anyone writes Out
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = r0 + wm + mi * 8 + g;
+          const int j = j0 + wn + ni * 8 + 2 * t + e;
+          if (r < n && j < b2) {
+            double* o = Out + r + (int64_t)j * ldo;
+            double v = alpha * acc[mi][ni][e];
+            if (beta != 0.0) v = fma(beta, *o, v);
+            *o = v;
+          }
+        }
+  }
+}
+
 // A (b x b, ld) <- upper triangle mirrored into the strict lower triangle
 __global__ void k_symm_upper(double* __restrict__ A, int b, int64_t ld) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
@@ -365,6 +490,21 @@ int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s) {
 static int g_nn_smem_set = 0;
 
 static size_t tn2_smem() { return (size_t)2 * TN_ST * V2_T * TN_P * sizeof(double); }
+static size_t nn3_smem(int b1) {
+  const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
+  return ((size_t)b1r * (V2_T + 4) + (size_t)2 * NN3_BN * V2_P) * sizeof(double);
+}
+// k_gemm_nn3 for inner dimensions above this (SCSF_NN3_MIN_K).  tools/gemm_bench.cu, n = 4e4:
+// b = 240: 20.1 against 16.4 TF/s (k_gemm_nn2); b = 120 (C2): 10.0 against 10.8, and C2 runs
+// 5-9 % slower with it, so the 4-warp kernel keeps b <= 128.
+static int nn3_min_k() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_NN3_MIN_K");
+    v = e ? atoi(e) : 128;
+  }
+  return v;
+}
 static size_t nn2_smem(int b1) {
   const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
   return ((size_t)b1r * (V2_T + 4) + (size_t)2 * V2_T * V2_P) * sizeof(double);
@@ -377,6 +517,8 @@ int dense_init_attrs() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn2_smem()));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn2_smem(NN2_MAX_K)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn3_smem(NN2_MAX_K)));
   g_nn_smem_set = 1;
   return SCSF_OK;
 }
@@ -467,7 +609,12 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(dense_init_attrs());
-  if (b1 <= NN2_MAX_K) {
+  if (b1 <= NN2_MAX_K && b1 > nn3_min_k() && b2 > V2_T) {
+    const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
+    const int m16 = ((ldm & 1) == 0 && ((uintptr_t)M & 15) == 0) ? 1 : 0;
+    k_gemm_nn3<<<ceil_div(n, V2_T), NN3_T, nn3_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
+                                                            a16, m16);
+  } else if (b1 <= NN2_MAX_K) {
     const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
     k_gemm_nn2<<<ceil_div(n, V2_T), V2_NT, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
                                                             a16);

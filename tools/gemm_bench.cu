@@ -2,6 +2,7 @@
 // CUDA events around R launches (no per-call synchronisation), TF/s against the 37 TF DMMA peak.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I. -o /tmp/gemm_bench tools/gemm_bench.cu
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -23,12 +24,14 @@ bool debug_sync() { return false; }
 using namespace scsf;
 
 int main() {
-  const int64_t n = 10000, ld = 10016;
+  const int64_t n = getenv("GB_N") ? atoll(getenv("GB_N")) : 10000;
+  const int64_t ld = (n + 31) / 32 * 32;
   const int R = 50;
   double *X, *Y, *M, *C, *P, *O;
   cudaMalloc(&X, ld * 400 * 8);
   cudaMalloc(&Y, ld * 400 * 8);
   cudaMalloc(&O, ld * 400 * 8);
+  const int BIG = getenv("GB_B") ? atoi(getenv("GB_B")) : 0;
   cudaMalloc(&M, 400 * 400 * 8);
   cudaMalloc(&C, 400 * 800 * 8);
   cudaMalloc(&P, tn_partial_doubles(n, 400, 400) * 8 + 1024);
@@ -45,6 +48,8 @@ int main() {
                              {"NN  n x 80 . 80 x 40 (BCGS)", 80, 40, 0}, {"TN  upper 120", 120, 120, 2},
                              {"TN  80 x 40 (BCGS)", 80, 40, 3}, {"TN  dual 120", 120, 120, 4},
                              {"NN  n x 56 . 56 x 56", 56, 56, 0}, {"TN  upper 56", 56, 56, 2}};
+  if (BIG) cases = {{"NN  n x B . B x B", BIG, BIG, 0}, {"NN  tri B", BIG, BIG, 1}, {"TN  upper B", BIG, BIG, 2},
+                    {"TN  dual B", BIG, BIG, 4}};
   for (auto& c : cases) {
     double flops = 2.0 * n * c.b1 * c.b2;
     if (c.kind == 1 || c.kind == 2) flops *= 0.5;
