@@ -139,7 +139,8 @@ constexpr int V2_NT = 128;                                 // threads per CTA
 // ---- TN: P[z] = X[kz, i-tile]^T Y[kz, j-tile]; upper: only tiles ti <= tj
 // TN pipeline: k-chunks of 16 in a 4-stage cp.async ring (3 chunks in flight): the Gram products
 // stream X and Y once with little reuse per CTA, so load latency, not DMMA, bounds a short chunk loop.
-constexpr int TN_KC = 16, TN_P = TN_KC + 4, TN_ST = 4;
+// Pitch 24 (= 8 mod 16 doubles): the 128-bit fragment loads below are conflict-free per quarter-warp.
+constexpr int TN_KC = 16, TN_P = TN_KC + 8, TN_ST = 4;
 
 __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X, int64_t ldx, int b1,
                                                   const double* __restrict__ Y, int64_t ldy, int b2, int64_t n,
@@ -206,19 +207,26 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
     if (c + TN_ST - 1 < nck) issue(c + TN_ST - 1, (c + TN_ST - 1) % TN_ST);
     cp_commit();
     const int stage = c % TN_ST;
-    const double* xa = xs + (stage * V2_T + wm + g) * TN_P + t;
-    const double* yb = ys + (stage * V2_T + wn + g) * TN_P + t;
+    // k pairs: lane (g, t) takes k = kk + 2t, kk + 2t + 1 with one 128-bit load and feeds them to
+    // two DMMAs as fragment k-index t (the same permutation of k on both operands: the sum over
+    // k is unchanged), halving the fragment load instructions
+    const double* xa = xs + (stage * V2_T + wm + g) * TN_P + 2 * t;
+    const double* yb = ys + (stage * V2_T + wn + g) * TN_P + 2 * t;
 #pragma unroll
-    for (int kk = 0; kk < TN_KC; kk += 4) {
-      double a[4], b[4];
+    for (int kk = 0; kk < TN_KC; kk += 8) {
+      double2 a[4], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * TN_P + kk];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = *reinterpret_cast<const double2*>(xa + mi * 8 * TN_P + kk);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = yb[ni * 8 * TN_P + kk];
+      for (int ni = 0; ni < 4; ++ni) b[ni] = *reinterpret_cast<const double2*>(yb + ni * 8 * TN_P + kk);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
     }
   }
   double* out = P + (int64_t)blockIdx.z * b1 * b2tot;
