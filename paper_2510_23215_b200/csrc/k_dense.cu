@@ -360,33 +360,37 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_nn2(const double* __restrict__ X
 // ---- NN, wide tile: Out[r0:r0+64, j0:j0+128] per pass with 8 warps (2 x 4 warp grid of 32 x 32).
 // For large b (C3-C5, V1: b = 240-360) k_gemm_nn2's 176-KB panel leaves one 4-warp CTA per SM
 // and sweeps the panel b/64 times; here 8 warps share the panel and it is swept b/128 times.
-constexpr int NN3_T = 256, NN3_BN = 128;
+constexpr int NN3_BN = 128;
 
-__global__ void __launch_bounds__(NN3_T) k_gemm_nn3(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
-                                                  const double* __restrict__ M, int64_t ldm, int b2,
-                                                  double alpha, double beta, double* Out, int64_t ldo,
-                                                  int tri_upper, int a16, int m16) {
+// PR = 64: 2 x 4 warps (256 threads); PR = 32: 1 x 4 warps (128 threads) with a 32-row panel,
+// so inner dimensions up to 384 fit (C5: b = 360) next to the 2-stage M ring.
+template <int PR>
+__global__ void __launch_bounds__(PR * 4) k_gemm_nn3(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
+                                                   const double* __restrict__ M, int64_t ldm, int b2,
+                                                   double alpha, double beta, double* Out, int64_t ldo,
+                                                   int tri_upper, int a16, int m16) {
+  constexpr int NT = PR * 4, PP = PR + 4;
   extern __shared__ __align__(16) double smd[];
   const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
-  double* xp = smd;                                  // [b1r][68]: xp[k*68 + r]
-  double* ms = smd + b1r * (V2_T + 4);               // [2][128][36]: ms[(st*128 + j)*36 + kk]
-  const int64_t r0 = (int64_t)blockIdx.x * V2_T;
+  double* xp = smd;                                  // [b1r][PR + 4]: xp[k*PP + r]
+  double* ms = smd + b1r * PP;                       // [2][128][36]: ms[(st*128 + j)*36 + kk]
+  const int64_t r0 = (int64_t)blockIdx.x * PR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;
   const int nck_all = b1r / V2_KC;
-  const int rows_here = (int)min((int64_t)V2_T, n - r0);
+  const int rows_here = (int)min((int64_t)PR, n - r0);
 
-  auto issue_panel = [&](int c) {      // 32 k-columns x 64 rows: 1024 16-byte segments
+  auto issue_panel = [&](int c) {      // 32 k-columns x PR rows of 16-byte segments
 #pragma unroll
-    for (int q = 0; q < 1024 / NN3_T; ++q) {
-      const int idx = tid + NN3_T * q;
-      const int kk = idx >> 5, seg = idx & 31;
+    for (int q = 0; q < 16 * PR / NT; ++q) {
+      const int idx = tid + NT * q;
+      const int kk = idx / (PR / 2), seg = idx % (PR / 2);
       const int k = c * V2_KC + kk;
       const int rr = 2 * seg;
       const int rem = (k < b1) ? max(0, min(2, rows_here - rr)) : 0;
       const double* src = rem ? X + r0 + rr + (int64_t)k * ldx : X;
-      double* dst = xp + k * (V2_T + 4) + rr;
+      double* dst = xp + k * PP + rr;
       if (a16) {
         cp_async16(dst, src, 8 * rem);
       } else {
@@ -398,8 +402,8 @@ __global__ void __launch_bounds__(NN3_T) k_gemm_nn3(const double* __restrict__ X
   auto issue_m = [&](int c, int j0, int stage) {   // 128 columns x 32 k
     if (m16) {
 #pragma unroll
-      for (int q = 0; q < 2048 / NN3_T; ++q) {
-        const int idx = tid + NN3_T * q;           // 0..2047
+      for (int q = 0; q < 2048 / NT; ++q) {
+        const int idx = tid + NT * q;              // 0..2047
         const int j = idx >> 4, seg = idx & 15;
         const int k = c * V2_KC + 2 * seg;
         const int rem = (j0 + j < b2) ? max(0, min(2, b1 - k)) : 0;
@@ -408,8 +412,8 @@ __global__ void __launch_bounds__(NN3_T) k_gemm_nn3(const double* __restrict__ X
       }
     } else {
 #pragma unroll 4
-      for (int q = 0; q < 4096 / NN3_T; ++q) {
-        const int idx = tid + NN3_T * q;           // 0..4095
+      for (int q = 0; q < 4096 / NT; ++q) {
+        const int idx = tid + NT * q;              // 0..4095
         const int j = idx >> 5, kk = idx & 31;
         const int k = c * V2_KC + kk;
         const bool ok = (k < b1) && (j0 + j < b2);
@@ -437,13 +441,13 @@ __global__ void __launch_bounds__(NN3_T) k_gemm_nn3(const double* __restrict__ X
       if (c + 1 < nck) cp_wait<1>();
       else cp_wait<0>();
       __syncthreads();
-      const double* xa = xp + (c * V2_KC + t) * (V2_T + 4) + wm + g;
+      const double* xa = xp + (c * V2_KC + t) * PP + wm + g;
       const double* mb = ms + ((c & 1) * NN3_BN + wn + g) * V2_P + t;
 #pragma unroll
       for (int kk = 0; kk < V2_KC; kk += 4) {
         double a[4], b[4];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * (V2_T + 4) + mi * 8];
+        for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * PP + mi * 8];
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) b[ni] = mb[ni * 8 * V2_P + kk];
 #pragma unroll
@@ -498,9 +502,9 @@ int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s) {
 static int g_nn_smem_set = 0;
 
 static size_t tn2_smem() { return (size_t)2 * TN_ST * V2_T * TN_P * sizeof(double); }
-static size_t nn3_smem(int b1) {
+static size_t nn3_smem(int b1, int pr) {
   const int b1r = (b1 + V2_KC - 1) / V2_KC * V2_KC;
-  return ((size_t)b1r * (V2_T + 4) + (size_t)2 * NN3_BN * V2_P) * sizeof(double);
+  return ((size_t)b1r * (pr + 4) + (size_t)2 * NN3_BN * V2_P) * sizeof(double);
 }
 // k_gemm_nn3 for inner dimensions above this (SCSF_NN3_MIN_K).  tools/gemm_bench.cu, n = 4e4:
 // b = 240: 20.1 against 16.4 TF/s (k_gemm_nn2); b = 120 (C2): 10.0 against 10.8, and C2 runs
@@ -510,6 +514,14 @@ static int nn3_min_k() {
   if (v < 0) {
     const char* e = getenv("SCSF_NN3_MIN_K");
     v = e ? atoi(e) : 128;
+  }
+  return v;
+}
+static int nn3_big() {                             // SCSF_NN3_BIG=0: the v1 kernel for b1 > 256
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_NN3_BIG");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v;
 }
@@ -525,8 +537,10 @@ int dense_init_attrs() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn2_smem()));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn2_smem(NN2_MAX_K)));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)nn3_smem(NN2_MAX_K)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn3_smem(NN2_MAX_K, 64)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn3_smem(NN_MAX_K, 32)));
   g_nn_smem_set = 1;
   return SCSF_OK;
 }
@@ -617,11 +631,14 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
     return SCSF_ERR_NOT_IMPLEMENTED;
   }
   SCSF_TRY(dense_init_attrs());
+  const int a16n = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
+  const int m16n = ((ldm & 1) == 0 && ((uintptr_t)M & 15) == 0) ? 1 : 0;
   if (b1 <= NN2_MAX_K && b1 > nn3_min_k() && b2 > V2_T) {
-    const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
-    const int m16 = ((ldm & 1) == 0 && ((uintptr_t)M & 15) == 0) ? 1 : 0;
-    k_gemm_nn3<<<ceil_div(n, V2_T), NN3_T, nn3_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,
-                                                            a16, m16);
+    k_gemm_nn3<64><<<ceil_div(n, 64), 256, nn3_smem(b1, 64), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
+                                                                 tri, a16n, m16n);
+  } else if (b1 > NN2_MAX_K && nn3_big()) {
+    k_gemm_nn3<32><<<ceil_div(n, 32), 128, nn3_smem(b1, 32), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
+                                                                 tri, a16n, m16n);
   } else if (b1 <= NN2_MAX_K) {
     const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
     k_gemm_nn2<<<ceil_div(n, V2_T), V2_NT, nn2_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo, tri,

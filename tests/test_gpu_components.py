@@ -54,7 +54,8 @@ def test_gemm_tn_upper(lib, n, b):
 
 
 @pytest.mark.parametrize("n,b1,b2,beta", [(10000, 120, 120, 0.0), (1001, 7, 130, -1.0), (333, 128, 33, 0.5),
-                                          (5000, 240, 240, 0.0), (64, 1, 1, 1.0)])
+                                          (5000, 240, 240, 0.0), (64, 1, 1, 1.0), (3001, 360, 360, 0.0),
+                                          (777, 300, 70, 1.0), (100, 257, 129, -0.5)])
 def test_gemm_nn(lib, n, b1, b2, beta):
     import torch
     rng = np.random.default_rng(n + b2)
@@ -70,7 +71,7 @@ def test_gemm_nn(lib, n, b1, b2, beta):
     assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
 
 
-@pytest.mark.parametrize("n,b", [(10000, 120), (4097, 64), (300, 240)])
+@pytest.mark.parametrize("n,b", [(10000, 120), (4097, 64), (300, 240), (2501, 360), (999, 300)])
 def test_gemm_nn_in_place(lib, n, b):
     rng = np.random.default_rng(b)
     X = rng.standard_normal((n, b))
