@@ -74,6 +74,7 @@ int grf_impl(int dim, int nx, int K, double s, double sigma, double vscale, int 
 // k_stencil.cu
 int assemble_vib_impl(const scsf_ops* ops, double h, const double* D, const double* rho, int64_t fstride,
                       double* coef, cudaStream_t s);
+int step_table_impl(double* fp, int m, cudaStream_t s);
 int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
                   const double* c, double* coef, cudaStream_t s);
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
@@ -114,7 +115,7 @@ static int check_solve_args(const scsf_ops* ops, int L, int nex, int degree, dou
   SCSF_ARG_CHECK(nex >= 0, "nex must be >= 0");
   SCSF_ARG_CHECK(L + nex <= n, "L + nex must be <= n");
   SCSF_ARG_CHECK(L + nex <= 368, "L + nex must be <= 368 in this build");
-  SCSF_ARG_CHECK(degree >= 1, "degree must be >= 1");
+  SCSF_ARG_CHECK(degree >= 1 && degree <= FP_MAX_DEGREE, "degree must be in [1, %d]", FP_MAX_DEGREE);
   SCSF_ARG_CHECK(tol > 0.0, "tol must be > 0");
   SCSF_ARG_CHECK(max_iter >= 0, "max_iter must be >= 0");
   return SCSF_OK;
@@ -237,7 +238,7 @@ size_t scsf_filter_workspace_bytes(const scsf_ops* ops, int32_t k, int64_t ldy) 
   if (!ops || k < 1) return 0;
   Arena a(nullptr, 0);
   a.take<double>(2 * ldy * k);
-  a.take<double>(4);
+  a.take<double>(FP_DOUBLES);
   return a.off;
 }
 
@@ -249,12 +250,12 @@ int scsf_cheb_filter(const scsf_ops* ops, int32_t op_index, const double* Y0, in
   SCSF_ARG_CHECK(op_index >= 0 && op_index < ops->n_ops, "op_index out of range");
   SCSF_ARG_CHECK(Y0 && Ym && Y0 != Ym, "Y0 / Ym NULL or aliased");
   SCSF_ARG_CHECK(k >= 1 && ldy >= n, "k >= 1 and ldy >= n required");
-  SCSF_ARG_CHECK(degree >= 1, "degree must be >= 1");
+  SCSF_ARG_CHECK(degree >= 1 && degree <= FP_MAX_DEGREE, "degree must be in [1, %d]", FP_MAX_DEGREE);
   SCSF_ARG_CHECK(e > 0.0 && lambda != c, "need e > 0 and lambda != c");
   Arena a(ws, ws_bytes);
   double* B1 = a.take<double>(ldy * k);
   double* B2 = a.take<double>(ldy * k);
-  double* fp = a.take<double>(4);
+  double* fp = a.take<double>(FP_DOUBLES);
   if (a.overflow || !ws) {
     set_error("workspace too small");
     return SCSF_ERR_WORKSPACE;
@@ -267,6 +268,7 @@ int scsf_cheb_filter(const scsf_ops* ops, int32_t op_index, const double* Y0, in
     SCSF_CUDA_CHECK(cudaStreamSynchronize(s));
     return SCSF_OK;
   }
+  SCSF_TRY(step_table_impl(fp, degree, s));
   // rotate over {Y0 (read-only), B1, B2, Ym}: Y_{s+1} never overwrites Y_s or Y_{s-1}
   const double* prev = nullptr;
   const double* cur = Y0;

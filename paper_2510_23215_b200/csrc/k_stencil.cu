@@ -80,27 +80,43 @@ __global__ void k_gershgorin(const double* __restrict__ cf, int dim, int nx, int
 }
 
 // ---------------------------------------------------- filter / SpMM step ----
-// fp = {lambda, c, e} (device).  step < 0: plain SpMM  Out = A X.
+// fp = {lambda, c, e, -, a_0, b_0, a_1, b_1, ...} (device; FP_DOUBLES).  step < 0: plain SpMM
+// Out = A X.  The per-step scalars a_s, b_s are tabulated once per filter by k_step_table
+// (step_table_impl, launched before the first step), so a step kernel reads two broadcast values
+// instead of every thread re-running the sigma recurrence up to its step (O(m) divisions each).
 __device__ __forceinline__ void step_scalars(const double* fp, int step, double& a, double& b,
                                              double& c) {
   if (step < 0) {
     a = 1.0; b = 0.0; c = 0.0;
     return;
   }
-  double lam = fp[0], cc = fp[1], e = fp[2];
-  double s1 = e / (lam - cc);
-  c = cc;
-  if (step == 0) {
-    a = s1 / e; b = 0.0;
-    return;
-  }
-  double sig = s1, prev = s1;
-  for (int i = 1; i <= step; ++i) {     // sigma_{i+1} = 1 / (2/sigma_1 - sigma_i)
-    prev = sig;
+  c = fp[1];
+  a = fp[FP_TAB + 2 * step];
+  b = fp[FP_TAB + 2 * step + 1];
+}
+
+// Alg. 1's scalars for steps 0..m-1 (one thread; the recurrence is sequential):
+//   a_0 = sigma_1 / e, b_0 = 0;  a_s = 2 sigma_{s+1} / e, b_s = -sigma_{s+1} sigma_s,
+//   sigma_1 = e / (lambda - c), sigma_{i+1} = 1 / (2 / sigma_1 - sigma_i).
+__global__ void k_step_table(double* fp, int m) {
+  if (threadIdx.x != 0) return;
+  const double lam = fp[0], cc = fp[1], e = fp[2];
+  const double s1 = e / (lam - cc);
+  fp[FP_TAB] = s1 / e;
+  fp[FP_TAB + 1] = 0.0;
+  double sig = s1;
+  for (int st = 1; st < m; ++st) {
+    const double prev = sig;
     sig = 1.0 / (2.0 / s1 - sig);
+    fp[FP_TAB + 2 * st] = 2.0 * sig / e;
+    fp[FP_TAB + 2 * st + 1] = -sig * prev;
   }
-  a = 2.0 * sig / e;
-  b = -sig * prev;
+}
+
+int step_table_impl(double* fp, int m, cudaStream_t s) {
+  k_step_table<<<1, 32, 0, s>>>(fp, m);
+  SCSF_LAUNCH_CHECK();
+  return SCSF_OK;
 }
 
 constexpr int ST_THREADS = 256;

@@ -53,6 +53,7 @@ int lock_impl(const double* theta, const double* res, const double* wn, double* 
               double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, cudaStream_t s);
 int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
 int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s);
+int step_table_impl(double* fp, int m, cudaStream_t s);
 int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s);
 int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncols, double* send_lo,
                    double* send_hi, cudaStream_t s);
@@ -104,7 +105,7 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.res = a.take<double>(b);
   w.wn = a.take<double>(b);
   w.rel = a.take<double>(b);
-  w.fp = a.take<double>(4);
+  w.fp = a.take<double>(FP_DOUBLES);
   w.perm = a.take<int>(b);
   w.ctrl = a.take<Ctrl>(1);
   w.gersh = a.take<unsigned long long>(1);
@@ -459,6 +460,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
                                     w.deg_on ? w.deg_on + kLc : nullptr));
       F = y[1];
     } else {
+      SCSF_TRY(step_table_impl(w.fp, degree, s));
       SCSF_TRY(spmm(ops, op, w, y[0], nullptr, y[1], ba, 0, s));
       for (int st_i = 1; st_i < degree; ++st_i)
         SCSF_TRY(spmm(ops, op, w, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], ba, st_i, s));
