@@ -1194,7 +1194,9 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
                    ((uintptr_t)X % 32 == 0) && ((uintptr_t)Out % 32 == 0) && ((uintptr_t)cf % 32 == 0) &&
                    (Xp == nullptr || (uintptr_t)Xp % 32 == 0);
   if (vec) {
-    constexpr int CB = 2;     // 2 columns per CTA: ~5x more CTAs than CB = 4, enough warps to hide latency
+    // 4 columns per CTA share each point's coefficient registers (tools/bench_filter.py, fraction of
+    // the HBM peak with CB = 2 / 4: C3 0.74 / 0.75, C4 (3-D) 0.60 / 0.68, C5 0.85 / 0.88)
+    constexpr int CB = 4;
     dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
     if (ops->dim == 2)
       k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
