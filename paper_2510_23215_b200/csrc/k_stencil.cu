@@ -937,7 +937,7 @@ int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, 
   if (ncols <= 0) return SCSF_OK;
   const int64_t n_glob = (int64_t)ops->nx * ops->ny;
   const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
-  constexpr int CB = 2;
+  constexpr int CB = 4;                // 4 columns per CTA share the coefficient registers
   dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
   k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
                                               ghost_lo, ghost_hi, fp, step);
