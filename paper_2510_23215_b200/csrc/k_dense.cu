@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // a warp whose 32 x 32 block lies outside b1 x b2, or (upper mode, diagonal tile) strictly below
+  // the diagonal, only helps load: consumers read the upper triangle, its entries stay 0
+  const bool idle = (i0 + wm >= b1) || (j0 + wn >= b2) || (upper && ti == tj && wm > wn);
 
 #pragma unroll
   for (int st = 0; st < TN_ST - 1; ++st) {
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
     // k is unchanged), halving the fragment load instructions
     const double* xa = xs + (stage * V2_T + wm + g) * TN_P + 2 * t;
     const double* yb = ys + (stage * V2_T + wn + g) * TN_P + 2 * t;
+    if (idle) continue;                              // warp-uniform
 #pragma unroll
     for (int kk = 0; kk < TN_KC; kk += 8) {
       double2 a[4], b[4];
