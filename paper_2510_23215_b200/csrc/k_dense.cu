@@ -318,8 +318,11 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_nn2(const double* __restrict__ X
       __syncthreads();
       const double* xa = xp + (c * V2_KC + t) * (V2_T + 4) + wm + g;
       const double* mb = ms + ((c & 1) * V2_T + wn + g) * V2_P + t;
+      // warp-uniform skips: columns past b2, or a triangular M whose rows of this chunk are all
+      // below the warp's columns (M[k][j] = 0 for k > j); the warp still loads and syncs
+      const bool idle = (j0 + wn >= b2) || (tri_upper && c * V2_KC > j0 + wn + 31);
 #pragma unroll
-      for (int kk = 0; kk < V2_KC; kk += 4) {
+      for (int kk = 0; kk < V2_KC && !idle; kk += 4) {
         double a[4], b[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * (V2_T + 4) + mi * 8];
@@ -447,8 +450,9 @@ __global__ void __launch_bounds__(PR * 4) k_gemm_nn3(const double* __restrict__ 
       __syncthreads();
       const double* xa = xp + (c * V2_KC + t) * PP + wm + g;
       const double* mb = ms + ((c & 1) * NN3_BN + wn + g) * V2_P + t;
+      const bool idle = (j0 + wn >= b2) || (tri_upper && c * V2_KC > j0 + wn + 31);   // as k_gemm_nn2
 #pragma unroll
-      for (int kk = 0; kk < V2_KC; kk += 4) {
+      for (int kk = 0; kk < V2_KC && !idle; kk += 4) {
         double a[4], b[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) a[mi] = xa[kk * PP + mi * 8];
