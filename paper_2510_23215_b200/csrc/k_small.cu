@@ -531,10 +531,14 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem) : "memory");
 }
 
+// Rows of Z transform independently, so a warp owns one row of the CTA's 16: per recorded round a
+// lane rotates its pair slots (lane, lane + 32) of that row and the warp only __syncwarp()s
+// between rounds; the CTA synchronises once per ZCH-round chunk of the record.
+constexpr int JZ_T = 512;
 template <int LOGB>
-__global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restrict__ rec, const int* __restrict__ recm,
-                                                        const int* __restrict__ nrec_p, const int* __restrict__ rank,
-                                                        int b, double* __restrict__ Zout) {
+__global__ void __launch_bounds__(JZ_T) k_jacobi_z(const double2* __restrict__ rec, const int* __restrict__ recm,
+                                                   const int* __restrict__ nrec_p, const int* __restrict__ rank,
+                                                   int b, double* __restrict__ Zout) {
   rec += (int64_t)blockIdx.y * JREC_SWEEPS * 128 * 64;      // batch: sub-problem blockIdx.y
   recm += blockIdx.y * JREC_SWEEPS * 128;
   nrec_p += blockIdx.y;
@@ -544,12 +548,12 @@ __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restric
   constexpr int H2 = B / 2;
   constexpr int R = 16;
   constexpr int ZP = B + 1;
-  constexpr int NT = H2 * R;
+  constexpr int NT = JZ_T;
+  constexpr int SPL = (H2 + 31) / 32;                       // pair slots per lane
   __shared__ double z[R * ZP];
   __shared__ __align__(16) double2 rs[2][ZCH * H2];
   __shared__ int ms[2][ZCH];
-  const int tid = threadIdx.x;
-  const int pslot = tid % H2, row = tid / H2;
+  const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
   const int x0 = blockIdx.x * R;
   for (int i = tid; i < R * B; i += NT) {
     const int r = i / B, cidx = i % B;
@@ -564,6 +568,7 @@ __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restric
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   if (nch > 0) load_chunk(0, 0);
+  double* zr = z + row * ZP;
   for (int ch = 0; ch < nch; ++ch) {
     const int buf = ch & 1;
     if (ch + 1 < nch) {
@@ -572,21 +577,27 @@ __global__ void __launch_bounds__(8 << LOGB) k_jacobi_z(const double2* __restric
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    __syncthreads();
+    __syncthreads();                                 // chunk ch visible; z rows initialised
     const int cnt = min(ZCH, nrec - ch * ZCH);
     for (int k = 0; k < cnt; ++k) {
-      const double2 cs = rs[buf][k * H2 + pslot];
-      if (cs.y != 0.0) {
-        const int m = ms[buf][k];
-        const int h = 31 - __clz(m);
-        const int lo = ins0(pslot, h), hi = lo ^ m;
-        double* zr = z + row * ZP;
-        const double zl = zr[lo], zh = zr[hi];
-        zr[lo] = cs.x * zl - cs.y * zh;
-        zr[hi] = cs.y * zl + cs.x * zh;
+      const int m = ms[buf][k];
+      const int h = 31 - __clz(m);
+#pragma unroll
+      for (int q = 0; q < SPL; ++q) {
+        const int pslot = lane + 32 * q;
+        if (pslot < H2) {
+          const double2 cs = rs[buf][k * H2 + pslot];
+          if (cs.y != 0.0) {
+            const int lo = ins0(pslot, h), hi = lo ^ m;
+            const double zl = zr[lo], zh = zr[hi];
+            zr[lo] = cs.x * zl - cs.y * zh;
+            zr[hi] = cs.y * zl + cs.x * zh;
+          }
+        }
       }
-      __syncthreads();
+      __syncwarp();                                  // this row's round k is complete
     }
+    __syncthreads();                                 // everyone is done with rs[buf] before it is refilled
   }
   for (int i = tid; i < R * B; i += NT) {
     const int r = i / B, cidx = i % B;
@@ -973,7 +984,7 @@ static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scra
   k_jacobi_g<LOGB><<<batch, 1024, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank,
                                                                      max_sweeps, ctrl, gstride, match);
   SCSF_LAUNCH_CHECK();
-  k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), 8 * B, 0, s>>>(rec, recm, nrec, rank, b, Zout);
+  k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), JZ_T, 0, s>>>(rec, recm, nrec, rank, b, Zout);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
