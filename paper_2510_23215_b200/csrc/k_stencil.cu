@@ -1023,12 +1023,18 @@ int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaSt
 }
 
 static int g_res_attr = 0;
+// The smallest cluster whose slabs fit, doubled once while slabs keep >= 8 rows: smaller CTAs
+// (C2: 14-row slabs, 350 threads, 102 KB) pack better next to the other chains' kernels
+// (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
+// clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
 static int cluster_size_for(const scsf_ops* ops) {
   if (ops->stencil != SCSF_STENCIL_FLUX || ops->dim != 2 || ops->nx % 2 != 0) return 0;
   for (int cs = 1; cs <= 8; cs *= 2) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
-    if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024)
-      return cs;
+    if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024) {
+      const int R2 = ((ops->ny + 2 * cs - 1) / (2 * cs) + 1) & ~1;
+      return (cs < 8 && R2 >= 8) ? 2 * cs : cs;
+    }
   }
   return 0;
 }
