@@ -347,8 +347,11 @@ __device__ __forceinline__ int ins0(int a, int h) {    // insert a 0 bit at posi
   return ((a & ~lowmask) << 1) | (a & lowmask);
 }
 
+// 512 threads: the kernel is latency-bound, and half the register file (and, with the TN tiles'
+// 3-stage ring, enough shared memory) stays free for the other chains' kernels on the same SM
+constexpr int JG_T = 512;
 template <int LOGB>
-__global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__ Gin, int64_t ldg, int b,
+__global__ void __launch_bounds__(JG_T, 1) k_jacobi_g(const double* __restrict__ Gin, int64_t ldg, int b,
                                                       double2* __restrict__ rec, int* __restrict__ recm,
                                                       int* __restrict__ nrec_out, double* __restrict__ theta_out,
                                                       int* __restrict__ rank_out, int max_sweeps, Ctrl* ctrl,
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
   const double tol = 1e-14, tol2 = tol * tol;
 
   double dmax = 0.0;
-  for (int idx = tid; idx < B * B; idx += 1024) {
+  for (int idx = tid; idx < B * B; idx += JG_T) {
     const int i = idx >> LOGB, j = idx & (B - 1);
     if (i <= j) {
       const double v = (i < b && j < b) ? Gin[i + (int64_t)j * ldg] : 0.0;
@@ -399,17 +402,17 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
   __syncthreads();
   if (tid == 0) {
     double v = 0.0;
-    for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+    for (int w = 0; w < JG_T / 32; ++w) v = fmax(v, red[w]);
     floor_s = 4.0 * 2.220446049250313e-16 * v;
   }
   __syncthreads();
   const double gfloor = floor_s;
-  // slot pairs (I <= J) of this thread: flat index k = tid + 1024 q over the upper triangle
-  constexpr int NBLK = H2 * (H2 + 1) / 2, JB_PER = (NBLK + 1023) / 1024;
+  // slot pairs (I <= J) of this thread: flat index k = tid + JG_T q over the upper triangle
+  constexpr int NBLK = H2 * (H2 + 1) / 2, JB_PER = (NBLK + JG_T - 1) / JG_T;
   int bI[JB_PER], bJ[JB_PER];
 #pragma unroll
   for (int q = 0; q < JB_PER; ++q) {
-    int k = q * 1024 + tid, I = 0;
+    int k = q * JG_T + tid, I = 0;
     while (I < H2 && k >= H2 - I) {                 // row I holds slots J = I .. H2-1
       k -= H2 - I;
       ++I;
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
   int sweep = 0;
   for (; sweep <= max_sweeps; ++sweep) {
     double mx = 0.0;
-    for (int i = warp; i < b; i += 32)
+    for (int i = warp; i < b; i += JG_T / 32)
       for (int j = i + 1 + lane; j < b; j += 32) {
         const double g = fabs(G[i * GP + j]);
         if (g > gfloor) mx = fmax(mx, g / fmax(sqrt(fabs(G[i * GP + i] * G[j * GP + j])), 1e-300));
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
     __syncthreads();
     if (tid == 0) {
       double v = 0.0;
-      for (int w = 0; w < 32; ++w) v = fmax(v, red[w]);
+      for (int w = 0; w < JG_T / 32; ++w) v = fmax(v, red[w]);
       red[0] = v;
     }
     __syncthreads();
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_g(const double* __restrict__
       // so a round costs a few index operations per block and no idle lanes.
 #pragma unroll
       for (int q = 0; q < JB_PER; ++q) {
-        if (q * 1024 + tid >= NBLK) break;
+        if (q * JG_T + tid >= NBLK) break;
         const int ilo = ins0(bI[q], h), jlo = ins0(bJ[q], h);
         const double2 cs1 = cs_cs[ilo], cs2 = cs_cs[jlo];
         if (cs1.y == 0.0 && cs2.y == 0.0) continue;
@@ -981,7 +984,7 @@ static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scra
   int* recm = reinterpret_cast<int*>(scratch + (size_t)batch * JREC_SWEEPS * 128 * 64 * 2);
   int* nrec = recm + batch * JREC_SWEEPS * 128;
   int* rank = nrec + 32;
-  k_jacobi_g<LOGB><<<batch, 1024, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank,
+  k_jacobi_g<LOGB><<<batch, JG_T, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank,
                                                                      max_sweeps, ctrl, gstride, match);
   SCSF_LAUNCH_CHECK();
   k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), JZ_T, 0, s>>>(rec, recm, nrec, rank, b, Zout);
