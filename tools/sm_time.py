@@ -14,7 +14,7 @@ import sys
 
 # resident CTAs per SM (from ptxas register / shared-memory use and block size)
 CTAS_PER_SM = {
-    "k_filter_cl": 1, "k_jacobi_g": 1, "k_jacobi_z": 1, "k_chol_reg": 1, "k_gemm_nn2": 2, "k_gemm_tn2": 3,
+    "k_filter_cl": 1, "k_filter_rp": 1, "k_gemm_nn3": 1, "k_jacobi_g": 1, "k_jacobi_z": 1, "k_chol_reg": 1, "k_gemm_nn2": 2, "k_gemm_tn2": 3,
     "k_reduce_partials": 8, "k_stencil_v4": 8, "k_resid": 4, "k_lock": 32, "k_gather_sign": 8,
 }
 
