@@ -72,3 +72,28 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), fn
+
+
+def test_new_queries_and_argument_errors_without_gpu(libpath):
+    """Session-3 entry points: size queries and argument validation need no device."""
+    from paper_2510_23215_b200 import scsf
+    lib = scsf.load_library(libpath)
+    ops = scsf.scsf_ops(2, 100, 100, 1, 10, 0, 10016, 1)
+    assert lib.scsf_chain_state_doubles(ctypes.byref(ops), 100, 20) == 120 * (10000 + 1)
+    assert lib.scsf_chain_state_doubles(ctypes.byref(ops), 0, 20) == 0
+    assert lib.scsf_grf_workspace_bytes(100, 16) == 2 * 16 * 101 * 8
+    # GRF: bad dim / K / family are rejected before any device work
+    assert lib.scsf_grf_fields(4, 10, 4, 1.0, 0.5, 1.0, 0, 1, None, None, None, None, None, None, None, 0,
+                               None) == scsf.SCSF_ERR_ARG
+    assert lib.scsf_grf_fields(2, 10, 33, 1.0, 0.5, 1.0, 0, 1, None, None, None, None, None, None, None, 0,
+                               None) == scsf.SCSF_ERR_ARG
+    assert lib.scsf_grf_fields(2, 10, 4, 1.0, 0.5, 1.0, 7, 1, None, None, None, None, None, None, None, 0,
+                               None) == scsf.SCSF_ERR_ARG
+    # vibration assembly: the stencil kind must be VIB13 and the grid 2-D with nx, ny >= 3
+    flux = scsf.scsf_ops(2, 8, 8, 1, 1, scsf.STENCIL_FLUX, 64, 1)
+    assert lib.scsf_assemble_vibration(ctypes.byref(flux), 0.1, 1, 1, 64, 1, None) == scsf.SCSF_ERR_ARG
+    vib3d = scsf.scsf_ops(3, 8, 8, 8, 1, scsf.STENCIL_VIB13, 512, 1)
+    assert lib.scsf_assemble_vibration(ctypes.byref(vib3d), 0.1, 1, 1, 512, 1, None) == scsf.SCSF_ERR_ARG
+    bad_kind = scsf.scsf_ops(2, 8, 8, 1, 1, 5, 64, 1)
+    assert lib.scsf_solve_workspace_bytes(ctypes.byref(bad_kind), 4, 1) >= 0
+    assert lib.scsf_assemble_vibration(ctypes.byref(bad_kind), 0.1, 1, 1, 64, 1, None) == scsf.SCSF_ERR_ARG
