@@ -52,11 +52,13 @@ def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
 @pytest.mark.parametrize("cfg_name,nx,k,m", [("C1", 32, 20, 20), ("C3", 29, 9, 7), ("C4", 11, 13, 20),
                                              ("C2", 40, 1, 1), ("C2", 100, 6, 20), ("C5", 110, 3, 5),
                                              ("C2", 92, 5, 20), ("C1", 132, 3, 20), ("C3", 76, 4, 9),
-                                             ("C2", 124, 2, 3), ("C1", 30, 5, 20), ("C3", 34, 3, 7)])
+                                             ("C2", 124, 2, 3), ("C1", 30, 5, 20), ("C3", 34, 3, 7),
+                                             ("C3", 200, 5, 20), ("C3", 190, 3, 9)])
 def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     """Both filter paths: resident (2-D: the register-patch kernel k_filter_rp when one CTA holds a
     column -- nx 30/32/34/40; 30 and 34 leave a 2-row top patch -- the cluster kernel with DSMEM
-    halos when a column fits 8 CTAs -- nx 92/100/132 give ragged row splits over 4 and 8 CTAs --
+    halos when a column fits 16 CTAs -- nx 92/100/132 give ragged row splits over 8 CTAs, nx 200/190
+    over 16 (a non-portable cluster) --
     else the single-CTA kernel for n <= 12288) and streaming (per-step launches, vectorised when
     nx % 4 == 0, scalar otherwise); SCSF_FILTER_STREAMING=1 forces streaming."""
     import torch
