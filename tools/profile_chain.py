@@ -20,9 +20,12 @@ def main():
     cfg = synth.get_config(name)
     f = synth.make_batch(cfg, nops)
     dev = torch.device("cuda", 0)
-    faces = [torch.from_numpy(x).to(dev) for x in f.faces]
-    ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).to(dev))
     params = torch.from_numpy(f.params).to(dev)
+    if f.is_vib:
+        ops = scsf.assemble_vibration(cfg.nx, cfg.h, params)
+    else:
+        faces = [torch.from_numpy(x).to(dev) for x in f.faces]
+        ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).to(dev))
     perm, _, _ = scsf.sort(params, cfg.dim, cfg.nx, cfg.p0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
