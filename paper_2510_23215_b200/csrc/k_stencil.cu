@@ -270,6 +270,78 @@ __global__ void __launch_bounds__(VB_THREADS) k_stencil_vib(
   }
 }
 
+// 13-point step with the row band staged in shared memory: a CTA owns VT_R grid rows for VT_CB
+// columns and stages those rows plus two halo rows each side of every column; every point then
+// reads its 12 neighbours from shared memory and its 13 coefficients through L1 once for all
+// VT_CB columns (k_stencil_vib reads every neighbour with its own 8-byte global load: ncu
+// long_scoreboard, 0.24 of the HBM rate on V1).  Flat-index neighbours wrap across row ends
+// exactly where the stencil's coefficients are zero, as in the DIA layout.  V1 (32 chains):
+// 11.8 -> 14.1 operators/s; staging the coefficients as well (56 KB per CTA) was slower (9.1),
+// and VT_R = 4 / 8 / 16 gave 13.2 / 13.9 / 14.1, VT_CB = 8 13.2.
+constexpr int VT_T = 256, VT_R = 16, VT_CB = 4;
+
+__global__ void __launch_bounds__(VT_T) k_stencil_vib_t(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
+                                                      const double* __restrict__ X, const double* Xp, double* Out,
+                                                      int64_t ldv, int ncols, const double* __restrict__ fp, int step) {
+  extern __shared__ __align__(16) double vs[];
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * VT_R, rows = min(VT_R, ny - r0);
+  const int j0 = blockIdx.y * VT_CB, ncb = min(VT_CB, ncols - j0);
+  const int n = nx * ny;
+  const int VW = (VT_R + 4) * nx;
+  double* sv = vs;                                  // [VT_CB][VW]: rows r0-2 .. r0+VT_R+1
+
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int vbase = (r0 - 2) * nx;
+  for (int i = tid; i < VW; i += VT_T) {
+    const int k = vbase + i;
+    const bool in = k >= 0 && k < n;
+#pragma unroll
+    for (int cc = 0; cc < VT_CB; ++cc)
+      sv[cc * VW + i] = (in && cc < ncb) ? __ldg(X + (int64_t)(j0 + cc) * ldv + k) : 0.0;
+  }
+  __syncthreads();
+  const int o2 = 2, o3 = nx - 1, o4 = nx, o5 = nx + 1, o6 = 2 * nx;
+  for (int i = tid; i < rows * nx; i += VT_T) {
+    const int lv = 2 * nx + i, lc = 2 * nx + i;    // local index of the point in sv / sc
+    const int64_t k = (int64_t)r0 * nx + i;
+    (void)lc;
+    const double* ck = cf + k;
+    const double dg = __ldg(ck) - c;
+    const double u1 = __ldg(ck + ldc), u2 = __ldg(ck + 2 * ldc), u3 = __ldg(ck + 3 * ldc), u4 = __ldg(ck + 4 * ldc),
+                 u5 = __ldg(ck + 5 * ldc), u6 = __ldg(ck + 6 * ldc);
+    const double l1 = k >= 1 ? __ldg(ck + ldc - 1) : 0.0, l2 = k >= o2 ? __ldg(ck + 2 * ldc - o2) : 0.0,
+                 l3 = k >= o3 ? __ldg(ck + 3 * ldc - o3) : 0.0, l4 = k >= o4 ? __ldg(ck + 4 * ldc - o4) : 0.0,
+                 l5 = k >= o5 ? __ldg(ck + 5 * ldc - o5) : 0.0, l6 = k >= o6 ? __ldg(ck + 6 * ldc - o6) : 0.0;
+#pragma unroll
+    for (int cc = 0; cc < VT_CB; ++cc) {
+      if (cc >= ncb) break;
+      const double* x = sv + cc * VW + lv;
+      double v = dg * x[0];
+      v = fma(u1, x[1], v);
+      v = fma(u2, x[o2], v);
+      v = fma(u3, x[o3], v);
+      v = fma(u4, x[o4], v);
+      v = fma(u5, x[o5], v);
+      v = fma(u6, x[o6], v);
+      v = fma(l1, x[-1], v);
+      v = fma(l2, x[-o2], v);
+      v = fma(l3, x[-o3], v);
+      v = fma(l4, x[-o4], v);
+      v = fma(l5, x[-o5], v);
+      v = fma(l6, x[-o6], v);
+      v *= a;
+      if (b != 0.0) v = fma(b, Xp[(int64_t)(j0 + cc) * ldv + k], v);
+      Out[(int64_t)(j0 + cc) * ldv + k] = v;
+    }
+  }
+  if (r0 + VT_R >= ny)                               // last band: the ld padding stays 0
+    for (int cc = 0; cc < ncb; ++cc)
+      for (int64_t k = n + tid; k < ldv; k += VT_T) Out[(int64_t)(j0 + cc) * ldv + k] = 0.0;
+}
+static size_t vib_t_smem(int nx) { return (size_t)(VT_CB * (VT_R + 4)) * nx * sizeof(double); }
+
 // Vectorised variant: 4 consecutive points per thread, 256-bit loads/stores of
 // the column streams (Y_s, Y_{s-1}, Y_{s+1}) and the coefficient arrays;
 // x-neighbours k-1 / k+4 as scalars (same cache lines), y/z-neighbours as
@@ -1120,6 +1192,7 @@ int stencil_init_attrs() {
   if (done) return SCSF_OK;
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * RES_MAX_N * (int)sizeof(double)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_stencil_vib_t, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define SCSF_CL_ATTR(CS, CB) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
   SCSF_CL_ATTR(1, 1); SCSF_CL_ATTR(1, 2); SCSF_CL_ATTR(1, 4);
@@ -1199,8 +1272,15 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
   const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
   if (ops->stencil == SCSF_STENCIL_VIB13) {
-    dim3 g(ceil_div(ldv, VB_THREADS), ceil_div(ncols, VB_COLS));
-    k_stencil_vib<<<g, VB_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n, X, Xp, Out, ldv, ncols, fp, step);
+    if (vib_t_smem(ops->nx) <= 200 * 1024) {
+      SCSF_TRY(stencil_init_attrs());
+      dim3 g(ceil_div(ops->ny, VT_R), ceil_div(ncols, VT_CB));
+      k_stencil_vib_t<<<g, VT_T, vib_t_smem(ops->nx), s>>>(cf, ops->ld, ops->nx, ops->ny, X, Xp, Out, ldv, ncols,
+                                                            fp, step);
+    } else {
+      dim3 g(ceil_div(ldv, VB_THREADS), ceil_div(ncols, VB_COLS));
+      k_stencil_vib<<<g, VB_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n, X, Xp, Out, ldv, ncols, fp, step);
+    }
     SCSF_LAUNCH_CHECK();
     return SCSF_OK;
   }
