@@ -1099,12 +1099,44 @@ static int g_res_attr = 0;
 // (C2: 14-row slabs, 350 threads, 102 KB) pack better next to the other chains' kernels
 // (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
 // clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
+int stencil_init_attrs();
+template <int CS, int CB>
+__global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
+                            int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
+                            const int* __restrict__ deg);
+// Can this device co-schedule a 16-CTA cluster of the largest filter CTA (768 threads, 200 KB)?
+// Checked once; a device that cannot (fewer SMs per GPC, partitioned GPUs) keeps clusters <= 8.
+static bool cs16_ok() {
+  static int v = -1;
+  if (v < 0) {
+    v = 0;
+    if (stencil_init_attrs() == SCSF_OK) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16, 1, 1);
+      cfg.blockDim = dim3(CL_T, 1, 1);
+      cfg.dynamicSmemBytes = 200 * 1024;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, k_filter_cl<16, 4>, &cfg) == cudaSuccess && nclusters > 0) v = 1;
+      cudaGetLastError();
+    }
+  }
+  return v == 1;
+}
+
 static int cluster_size_for(const scsf_ops* ops) {
   if (ops->stencil != SCSF_STENCIL_FLUX || ops->dim != 2 || ops->nx % 2 != 0) return 0;
   // up to 16 CTAs (a non-portable cluster size, opted in per kernel): C3's 200 x 200 slabs fit at
   // 16 (7 x 100 patches, 4 columns per CTA) and the whole filter stays on chip: 1.05 of the HBM
   // roofline's algorithmic rate against 0.74 for the streaming kernel; C3 8.7 -> 9.9 ops/s
-  for (int cs = 1; cs <= 16; cs *= 2) {
+  const int cs_max = cs16_ok() ? 16 : 8;
+  for (int cs = 1; cs <= cs_max; cs *= 2) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024) {
       const int R2 = ((ops->ny + 2 * cs - 1) / (2 * cs) + 1) & ~1;
