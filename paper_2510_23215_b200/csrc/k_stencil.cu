@@ -928,6 +928,122 @@ __global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict_
   }
 }
 
+// W = A V fused with the residual norms of Alg. 3 l. 7: per column j the squared norms of
+// w - theta_j v and of w are summed per CTA (fixed order) into partials P[(2 j + {0,1}) nblk + cta]
+// and k_resid_sum adds the nblk partials in ascending order.  W itself is never written (after
+// the rotation it only feeds the residuals).  nx % 4 == 0 (no tail quads); padding adds 0.
+template <int DIM, int CB>
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_resid(
+    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n, const double* __restrict__ X,
+    int64_t ldv, int ncols, const double* __restrict__ theta, double* __restrict__ P, int nblk) {
+  const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
+  const int64_t sxy = (int64_t)nx * ny;
+  const int j0 = blockIdx.y * CB;
+  double rr[CB], ww[CB];
+#pragma unroll
+  for (int jj = 0; jj < CB; ++jj) rr[jj] = ww[jj] = 0.0;
+  if (k0 + 4 <= n) {
+    const double4 dg = ldg4_nc(cf + k0);
+    const double4 cxp = ldg4_nc(cf + ldc + k0);
+    const double cxm = (k0 >= 1) ? cf[ldc + k0 - 1] : 0.0;
+    const double4 cyp = ldg4_nc(cf + 2 * ldc + k0);
+    const bool hym = k0 >= nx, hyp = k0 + nx + 3 < n;
+    const double4 cym = hym ? ldg4_nc(cf + 2 * ldc + k0 - nx) : make_double4(0, 0, 0, 0);
+    double4 czp = make_double4(0, 0, 0, 0), czm = make_double4(0, 0, 0, 0);
+    bool hzm = false, hzp = false;
+    if (DIM == 3) {
+      czp = ldg4_nc(cf + 3 * ldc + k0);
+      hzm = k0 >= sxy;
+      hzp = k0 + sxy + 3 < n;
+      if (hzm) czm = ldg4_nc(cf + 3 * ldc + k0 - sxy);
+    }
+    const bool hm = k0 >= 1, hp = k0 + 4 < n;
+#pragma unroll
+    for (int jj = 0; jj < CB; ++jj) {
+      const int j = j0 + jj;
+      if (j >= ncols) break;
+      const double* __restrict__ x = X + (int64_t)j * ldv;
+      const double4 xc = ldg4_nc(x + k0);
+      const double xl = hm ? x[k0 - 1] : 0.0;
+      const double xr = hp ? x[k0 + 4] : 0.0;
+      const double4 xu = hyp ? ldg4_nc(x + k0 + nx) : make_double4(0, 0, 0, 0);
+      const double4 xd = hym ? ldg4_nc(x + k0 - nx) : make_double4(0, 0, 0, 0);
+      double4 v;
+      v.x = dg.x * xc.x + cxp.x * xc.y + cxm * xl + cyp.x * xu.x + cym.x * xd.x;
+      v.y = dg.y * xc.y + cxp.y * xc.z + cxp.x * xc.x + cyp.y * xu.y + cym.y * xd.y;
+      v.z = dg.z * xc.z + cxp.z * xc.w + cxp.y * xc.y + cyp.z * xu.z + cym.z * xd.z;
+      v.w = dg.w * xc.w + cxp.w * xr + cxp.z * xc.z + cyp.w * xu.w + cym.w * xd.w;
+      if (DIM == 3) {
+        const double4 zu = hzp ? ldg4_nc(x + k0 + sxy) : make_double4(0, 0, 0, 0);
+        const double4 zd = hzm ? ldg4_nc(x + k0 - sxy) : make_double4(0, 0, 0, 0);
+        v.x += czp.x * zu.x + czm.x * zd.x;
+        v.y += czp.y * zu.y + czm.y * zd.y;
+        v.z += czp.z * zu.z + czm.z * zd.z;
+        v.w += czp.w * zu.w + czm.w * zd.w;
+      }
+      const double th = theta[j];
+      const double d0 = fma(-th, xc.x, v.x), d1 = fma(-th, xc.y, v.y), d2 = fma(-th, xc.z, v.z),
+                   d3 = fma(-th, xc.w, v.w);
+      rr[jj] = fma(d0, d0, fma(d1, d1, fma(d2, d2, d3 * d3)));
+      ww[jj] = fma(v.x, v.x, fma(v.y, v.y, fma(v.z, v.z, v.w * v.w)));
+    }
+  }
+  __shared__ double red[2 * CB][SV_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int jj = 0; jj < CB; ++jj) {
+    const double r = warp_sum(rr[jj]), w = warp_sum(ww[jj]);
+    if (lane == 0) {
+      red[2 * jj][warp] = r;
+      red[2 * jj + 1][warp] = w;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * CB) {
+    const int jj = threadIdx.x >> 1, j = j0 + jj;
+    if (j < ncols) {
+      double t = 0.0;
+      for (int q = 0; q < SV_THREADS / 32; ++q) t += red[threadIdx.x][q];
+      P[(int64_t)(2 * j + (threadIdx.x & 1)) * nblk + blockIdx.x] = t;
+    }
+  }
+}
+
+__global__ void k_resid_sum(const double* __restrict__ P, int nblk, double* __restrict__ res, double* __restrict__ wn) {
+  const int j = blockIdx.x;
+  if (threadIdx.x >= 2) return;
+  const double* p = P + (int64_t)(2 * j + threadIdx.x) * nblk;
+  double t = 0.0;
+  for (int q = 0; q < nblk; ++q) t += p[q];
+  if (threadIdx.x == 0) res[j] = t;
+  else wn[j] = t;
+}
+
+// Residual norms from V without materialising W = A V (flux stencils, nx % 4 == 0, no row
+// partition); returns false when the caller must use stencil_impl + resid_impl instead.
+int stencil_resid_impl(const scsf_ops* ops, int op, const double* V, int64_t ldv, int ncols, const double* theta,
+                       double* res, double* wn, double* P, cudaStream_t s, bool* done) {
+  *done = false;
+  if (ncols <= 0) { *done = true; return SCSF_OK; }
+  const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
+  if (ops->stencil != SCSF_STENCIL_FLUX || ops->nx % 4 != 0 || ldv % 4 != 0 || ops->ld % 4 != 0 ||
+      ((uintptr_t)V % 32) != 0 || ((uintptr_t)cf % 32) != 0)
+    return SCSF_OK;
+  const int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
+  constexpr int CB = 4;
+  const int nblk = (int)ceil_div(ceil_div(ldv, 4), SV_THREADS);
+  dim3 g(nblk, ceil_div(ncols, CB));
+  if (ops->dim == 2)
+    k_stencil_resid<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, V, ldv, ncols, theta, P, nblk);
+  else
+    k_stencil_resid<3, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, V, ldv, ncols, theta, P, nblk);
+  SCSF_LAUNCH_CHECK();
+  k_resid_sum<<<ncols, 32, 0, s>>>(P, nblk, res, wn);
+  SCSF_LAUNCH_CHECK();
+  *done = true;
+  return SCSF_OK;
+}
+
 // ------------------------------------------------ row-partitioned (slab) ----
 // Row partition of a 2-D operator: this rank owns grid rows
 // [y0, y1); vectors hold only those n_loc = nx (y1 - y0) rows, the operator

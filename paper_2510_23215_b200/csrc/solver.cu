@@ -31,6 +31,8 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
 bool filter_resident_ok(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
                          const double* fp, int m, cudaStream_t s, const int* deg = nullptr);
+int stencil_resid_impl(const scsf_ops* ops, int op, const double* V, int64_t ldv, int ncols, const double* theta,
+                       double* res, double* wn, double* P, cudaStream_t s, bool* done);
 int resid_impl(const double* V, const double* W, int64_t ldv, int64_t n, int ncols,
                const double* theta, double* res, double* wn, cudaStream_t s);
 int gershgorin_impl(const scsf_ops* ops, int op, unsigned long long* out, cudaStream_t s);
@@ -197,6 +199,15 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
 // Rayleigh-Ritz step (Q2 Z = Q1 (R2^{-1} Z)); it saves one n x b pass (the
 // second triangular apply) and fuses two Gram passes into one.  The b x b
 // products are replicated (identical on every rank of a row partition).
+static bool fused_resid() {                         // SCSF_FUSED_RESID=0: W = A V then k_resid
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_FUSED_RESID");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int L, double tol, cudaStream_t s) {
   const int ba = w.b - k0;
   const int64_t bb = (int64_t)ba * ba;
@@ -214,9 +225,15 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
   SCSF_TRY(gemm_nn_ex(w.Rinv, ba, ba, ba, w.Zs, ba, ba, 1.0, 0.0, w.Mb, ba, 0, s));        // M = R2^{-1} Z
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Va, w.ldv, s));
-  // W = A V by one stencil pass (cheaper than the n x b x b product W1 M; only the residuals use it)
-  SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
-  SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
+  // residuals of A V by one stencil pass (cheaper than the n x b x b product W1 M); without a row
+  // partition the pass is fused with the norms and W is not written (only the residuals use it)
+  bool fused = false;
+  if (!w.comm && fused_resid())
+    SCSF_TRY(stencil_resid_impl(ops, op, Va, w.ldv, ba, w.theta + k0, w.res + k0, w.wn + k0, w.P, s, &fused));
+  if (!fused) {
+    SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
+    SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
+  }
   if (w.comm) {
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
     SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
