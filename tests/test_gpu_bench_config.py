@@ -83,3 +83,27 @@ def test_c2_full_queue_32_chains(lib):
         check_pairs(f, op, ev[k], evecs[k, :, :n].cpu().numpy().T, cfg.L, paper_tol=10 * cfg.tol)
     lo, hi = checks.loewner_bounds(f, int(perm[0]), cfg.L)
     assert np.all(lo <= ev[0] * (1 + 1e-12)) and np.all(ev[0] <= hi * (1 + 1e-12))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_queue_properties(lib, name):
+    """configs[2] / configs[3] at full N through scsf_solve_chains (32 chains): every operator
+    converges to the paper metric, its Ritz values ascend and sit inside the Courant-Fischer
+    (Loewner) bounds of its coefficients; properties that hold at any size (the eigenvectors of
+    400 x 40000 x 200 would not fit a test)."""
+    import torch
+    cfg = synth.get_config(name)
+    f = synth.make_batch(cfg)
+    ops, params = device_problem(f)
+    perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
+    evals, _, stats = lib.solve_chains(ops, perm, 32, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=2,
+                                       want_vecs=False)
+    torch.cuda.synchronize()
+    assert len(stats) == cfg.n_ops
+    assert all(s["status"] == 0 for s in stats)
+    assert max(s["max_rel_resid"] for s in stats) <= 10 * cfg.tol
+    ev = evals.cpu().numpy()
+    assert np.all(np.diff(ev, axis=1) >= 0)
+    for k in range(len(perm)):
+        lo, hi = checks.loewner_bounds(f, int(perm[k]), cfg.L)
+        assert np.all(lo <= ev[k] * (1 + 1e-12)) and np.all(ev[k] <= hi * (1 + 1e-12)), k
