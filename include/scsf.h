@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SCSF_ABI_VERSION 1
+#define SCSF_ABI_VERSION 2
 
 typedef enum {
   SCSF_OK = 0,
@@ -100,6 +100,10 @@ typedef struct {
   double filter_bytes;       /* algorithmic HBM bytes of the filter steps */
   int32_t jacobi_sweeps;     /* reduced-eigensolver sweeps, summed over RR steps      */
   int32_t reserved0;
+  double t_gemm_ms;          /* tall-skinny DGEMM tiles (Gram / projection / rotation),
+                                CUDA events around each launch (0 unless timing is on)  */
+  double gemm_flops;         /* their algorithmic flops (upper-triangle Grams: unique
+                                entries; triangular R^-1: half) (0 unless timing is on) */
 } scsf_stats;
 
 /* ---------------------------------------------------------------- sort ---- */
@@ -216,7 +220,15 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  * ChFSI for one operator, Alg. 3: the L smallest eigenpairs of
  * A^(op_index) to relative residual ||Av - lv||/||Av|| <= tol.
  *  nex       extra (inherited) subspace columns: block b = L + nex (R12)
- *  degree    Chebyshev filter degree m (default 20)
+ *  degree    Chebyshev filter degree m (default 20).  m in [1, 128]: every active
+ *            column is filtered with degree m (reading R8).  m in [-128, -4]: per-column
+ *            degrees (Alg. 1 l. 5's staggered update, the ChASE-style
+ *            variant the paper cites): after each Rayleigh-Ritz step column j gets
+ *            the degree its residual and Ritz value need to reach 0.1 tol, clamped to
+ *            [4, |m|]; finished columns are left untouched by the remaining steps.
+ *            Honoured by the resident filters and the vectorised streaming step
+ *            (5-/7-point operators, nx % 4 == 0); elsewhere (13-point family, row
+ *            partition) it falls back to the uniform degree |m|.
  *  max_iter  outer-iteration cap (R24; 200)
  *  warm_vecs dev [b][ld_vec] or NULL: initial block V~_0 ("V~_0 = V^(i-1)");
  *            NULL = seeded Gaussian start (R17), seed + op_index.
@@ -225,7 +237,8 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  *            entry positive, R21); may alias warm_vecs.
  *  ld_vec    leading dimension of warm_vecs / evecs (>= n).
  *  st        host out (may be NULL).
- * Errors: SCSF_ERR_ARG (L < 1, nex < 0, L + nex > n, degree < 1, tol <= 0),
+ * Errors: SCSF_ERR_ARG (L < 1, nex < 0, L + nex > n, degree outside [1, 128] and
+ * [-128, -4], tol <= 0),
  * SCSF_ERR_WORKSPACE, SCSF_ERR_NUMERICAL (not converged; outputs hold the
  * best pairs found and st->max_rel_resid the worst residual).
  */
@@ -237,8 +250,12 @@ int scsf_solve_one(const scsf_ops* ops, int32_t op_index, int32_t L, int32_t nex
 /*
  * SCSF sequential solve along a sorted chain (Fig. 2 d1-d3):
  * operator chain[0] starts from a seeded random block, every later one from
- * the previous operator's final b-block (warm start, R11: one Rayleigh-Ritz
- * on the new operator before the first filter).
+ * the previous operator's final b-block (warm start).  Reading R11 (P:193-194,
+ * P:297 "Lambda~_0 = Lambda^(i-1)"): the first filter of a warm solve uses the
+ * previous operator's Ritz values as its bounds (lambda = theta_1, alpha =
+ * theta_b) with the new operator's Gershgorin beta; the first Rayleigh-Ritz
+ * follows that filter.  The process-wide switch SCSF_INHERIT_BOUNDS=0 restores
+ * one Rayleigh-Ritz of the new operator before the first filter.
  *  chain   host [n_chain]: operator indices in solve order (a slice of scsf_sort's perm)
  *  evals   dev [n_chain][L] out, by chain position
  *  evecs   dev [n_chain][L][ld_vec] out or NULL
@@ -406,9 +423,10 @@ const char* scsf_last_error(void);   /* thread-local message for the last non-OK
 int scsf_abi_version(void);          /* SCSF_ABI_VERSION                                */
 int64_t scsf_launch_count(void);     /* kernels launched by this process so far         */
 int scsf_set_timing(int32_t on);     /* enable per-phase CUDA-event timers; returns the old state */
-/* which Alg. 1 kernel the solver uses for these operators: 2 = cluster-resident
- * whole filter (k_filter_cl), 1 = single-CTA resident (k_filter_res2d), 0 = one
- * streaming launch per step (k_stencil_v4); -1 = invalid ops */
+/* which Alg. 1 kernel the solver uses for these operators: 3 = register-patch
+ * cluster-resident whole filter (k_filter_rp), 2 = cluster-resident whole filter
+ * (k_filter_cl), 1 = single-CTA resident (k_filter_res2d), 0 = one streaming
+ * launch per step (k_stencil_v4 / k_stencil / k_stencil_vib_t); -1 = invalid ops */
 int scsf_filter_kind(const scsf_ops* ops);
 
 #ifdef __cplusplus

@@ -9,12 +9,20 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
   subspace_sine     ||(I - U U^T) V||_2  (direct sine, not sqrt(1 - cos^2))
   inertia_below     Sylvester inertia: #eigenvalues of A below sigma, counted as
                     the negative pivots of a no-pivot banded LDL^T of A - sigma I
+  inertia_blocks    the same count by block Gaussian elimination over the grid's
+                    block-tridiagonal structure (blocks of u = largest stencil
+                    stride unknowns): inertia(A - sigma I) = sum_i inertia(S_i),
+                    S_0 = D_0 - sigma I, S_i = D_i - sigma I - E_i S_{i-1}^{-1} E_i^T
+                    (Haynsworth inertia additivity of the Schur complement); each
+                    S_i's count from a Bunch-Kaufman LDL^T (scipy.linalg.ldl, a
+                    library primitive).  Used for O8 at C3-C5 sizes.
   loewner_bounds    a_min lam_j(L0) + c_min <= lam_j(A) <= a_max lam_j(L0) + c_max
                     (Courant-Fischer; flux form is monotone in the face coefficients)
 """
 from __future__ import annotations
 
 import numpy as np
+import scipy.linalg as sla
 
 from . import operator as op
 
@@ -105,6 +113,40 @@ def inertia_below(fields, i, sigma: float) -> int:
             vals[u] = 1.0
         W[u, :] = vals
         W[:, u] = vals
+    return neg
+
+
+def _negative_count(S: np.ndarray) -> int:
+    """#negative eigenvalues of dense symmetric S from its LDL^T (Sylvester: inertia(S) = inertia(D))."""
+    _, d, _ = sla.ldl(S, lower=True)
+    # D is block diagonal with 1x1 and 2x2 blocks: a symmetric tridiagonal matrix
+    w = sla.eigvalsh_tridiagonal(np.diag(d).copy(), np.diag(d, -1).copy())
+    return int(np.sum(w < 0.0))
+
+
+def inertia_blocks(fields, i, sigma: float) -> int:
+    """Number of eigenvalues of A^(i) below sigma by block LDL^T of A - sigma I.
+
+    With u = the largest stencil stride, A couples unknowns at most u apart, so in
+    consecutive blocks of u unknowns A is block tridiagonal (diagonal blocks D_i,
+    sub-diagonal blocks E_i = A[block i, block i-1]).  Block elimination without
+    block pivoting gives A - sigma I = L diag(S_0, S_1, ...) L^T, so by Sylvester's
+    law of inertia the count is the sum of the negative counts of the S_i.
+    """
+    A = op.assemble_csr(fields, i)
+    n = A.shape[0]
+    u = op.strides(fields)[-1]
+    S_prev = None
+    neg = 0
+    for r0 in range(0, n, u):
+        r1 = min(n, r0 + u)
+        S = A[r0:r1, r0:r1].toarray() - sigma * np.eye(r1 - r0)
+        if S_prev is not None:
+            E = A[r0:r1, r0 - u:r0].toarray()           # rows of this block, columns of the previous one
+            S = S - E @ np.linalg.solve(S_prev, E.T)
+            S = 0.5 * (S + S.T)
+        neg += _negative_count(S)
+        S_prev = S
     return neg
 
 

@@ -17,7 +17,9 @@ and warm start.  Every configuration is SPD (R20), so "smallest
                      size 8 so (near-)degenerate eigenvalues are captured;
                      the small projected matrix is diagonalised by numpy.eigh
                      (library primitive); Ritz pairs are accepted on the TRUE
-                     residual ||A v - lambda v|| computed with A itself.
+                     residual ||A v - lambda v|| computed with A itself, and
+                     the function RAISES (OracleNotConverged) rather than
+                     return a pair above that bound.
 """
 from __future__ import annotations
 
@@ -66,6 +68,10 @@ def jacobi_eigh(A: np.ndarray, tol: float = 1e-15, max_sweeps: int = 100):
     w = np.diag(A).copy()
     idx = np.argsort(w, kind="stable")
     return w[idx], V[:, idx], sweeps
+
+
+class OracleNotConverged(RuntimeError):
+    """smallest_eigpairs hit its Krylov cap before every wanted pair met its residual bound."""
 
 
 class SolveResult:
@@ -142,8 +148,14 @@ def smallest_eigpairs(fields, i, k: int, block: int = 8, seed: int = 7,
             R = AV - Vk * lam
             res = np.linalg.norm(R, axis=0)
             tol = np.maximum(rtol * np.abs(lam), floor_rel * normA)
-            if np.all(res <= tol) or done:
+            if np.all(res <= tol):
                 idx = np.argsort(lam, kind="stable")
                 return SolveResult(lam[idx], Vk[:, idx], res[idx], m, normA)
+            if done:
+                # never hand back unconverged pairs as the reference
+                bad = int(np.sum(res > tol))
+                raise OracleNotConverged(
+                    f"operator {i}: {bad} of {k} pairs above max({rtol:g} |lam|, {floor_rel:g} ||A||) "
+                    f"at Krylov dimension {m} (worst ||r|| / bound = {float(np.max(res / tol)):.3e})")
         Qbuf[:, (j + 1) * block:(j + 2) * block] = Xn
         j += 1

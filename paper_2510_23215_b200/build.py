@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libscsf.so")
-SOURCES = ["api.cu", "solver.cu", "comm.cu", "k_sort.cu", "k_stencil.cu", "k_dense.cu", "k_small.cu", "k_blockjac.cu", "k_grf.cu"]
+SOURCES = ["api.cu", "solver.cu", "comm.cu", "k_sort.cu", "k_stencil.cu", "k_dense.cu", "k_small.cu", "k_blockjac.cu", "k_grf.cu", "graph_loop.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

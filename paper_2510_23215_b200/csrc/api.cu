@@ -78,7 +78,7 @@ int step_table_impl(double* fp, int m, cudaStream_t s);
 int assemble_impl(const scsf_ops* ops, double h, const double* fx, const double* fy, const double* fz,
                   const double* c, double* coef, cudaStream_t s);
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out, int64_t ldv,
-                 int ncols, const double* fp, int step, cudaStream_t s);
+                 int ncols, const double* fp, int step, cudaStream_t s, const int* deg = nullptr);
 bool filter_resident_ok(const scsf_ops* ops);
 int filter_kind(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
@@ -115,7 +115,9 @@ static int check_solve_args(const scsf_ops* ops, int L, int nex, int degree, dou
   SCSF_ARG_CHECK(nex >= 0, "nex must be >= 0");
   SCSF_ARG_CHECK(L + nex <= n, "L + nex must be <= n");
   SCSF_ARG_CHECK(L + nex <= 368, "L + nex must be <= 368 in this build");
-  SCSF_ARG_CHECK(degree >= 1 && degree <= FP_MAX_DEGREE, "degree must be in [1, %d]", FP_MAX_DEGREE);
+  SCSF_ARG_CHECK((degree >= 1 && degree <= FP_MAX_DEGREE) || (degree <= -4 && degree >= -FP_MAX_DEGREE),
+                 "degree must be in [1, %d] (uniform) or [-%d, -4] (per-column adaptive, cap |degree|)",
+                 FP_MAX_DEGREE, FP_MAX_DEGREE);
   SCSF_ARG_CHECK(tol > 0.0, "tol must be > 0");
   SCSF_ARG_CHECK(max_iter >= 0, "max_iter must be >= 0");
   return SCSF_OK;

@@ -112,3 +112,33 @@ struct Ctrl {
 };
 
 }  // namespace scsf
+
+// ------------------------------------------------ device-side loops ----
+// A loop whose continuation is decided on the device.  On a stream that is being
+// captured into a CUDA graph the loop becomes a WHILE conditional node: its body is
+// captured once on a side stream into the node's body graph, and the body's last
+// kernel sets the condition (dev_loop_continue), so a replay runs as many passes as
+// the data needs without the host.  Outside a capture the same body is launched
+// pass by pass and the host reads the flag the deciding kernel also writes.
+namespace scsf {
+struct DevLoop {
+  cudaGraphConditionalHandle handle = 0;
+  int in_graph = 0;         // 1: set the conditional; 0: only the flag word
+  int* flag = nullptr;      // device int written with the decision either way
+};
+__device__ __forceinline__ void dev_loop_continue(const DevLoop& L, bool more) {
+  *L.flag = more ? 1 : 0;
+  if (L.in_graph) cudaGraphSetConditional(L.handle, more ? 1u : 0u);
+}
+bool stream_capturing(cudaStream_t s);
+int take_cond_kernels();     // kernels of conditional bodies captured on this thread since the last call
+// body(cudaStream_t bs, const DevLoop& L) -> int status; runs while the device says so
+// (at least once).  flag_d: one device int; flag_h: one pinned host int (eager mode).
+int device_while_impl(cudaStream_t s, int* flag_d, int* flag_h, int (*body)(cudaStream_t, const DevLoop&, void*),
+                      void* ctx, int max_passes_eager);
+template <class F>
+int device_while(cudaStream_t s, int* flag_d, int* flag_h, int max_passes_eager, F& body) {
+  auto tramp = [](cudaStream_t bs, const DevLoop& L, void* c) -> int { return (*static_cast<F*>(c))(bs, L); };
+  return device_while_impl(s, flag_d, flag_h, tramp, &body, max_passes_eager);
+}
+}  // namespace scsf

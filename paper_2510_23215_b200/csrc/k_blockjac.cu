@@ -13,6 +13,7 @@
 // |g_ij| <= 1e-14 sqrt|g_ii g_jj| (as the one-CTA Jacobi).
 #include "common.cuh"
 
+#include <mutex>
 #include <vector>
 
 namespace scsf {
@@ -44,8 +45,9 @@ __global__ void __launch_bounds__(512) k_bj_bound(const double* __restrict__ G, 
 // (zero off-diagonal) with a diagonal above the whole spectrum (2 x the Gershgorin bound + 1),
 // so every sorted sub-solve keeps them last, i.e. at their own positions.
 __global__ void k_bj_load(const double* __restrict__ G, int64_t ldg, int b, int n, const double* __restrict__ bound,
-                          double* __restrict__ Gp, double* __restrict__ Zp) {
+                          double* __restrict__ Gp, double* __restrict__ Zp, int* __restrict__ counter) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i == 0 && j == 0) *counter = 0;                 // sweeps of this solve
   if (i >= n) return;
   double v = 0.0;
   if (i < b && j < b) v = (i <= j) ? G[i + (int64_t)j * ldg] : G[j + (int64_t)i * ldg];
@@ -96,10 +98,16 @@ __global__ void __launch_bounds__(256) k_bj_blkmm(const double* __restrict__ X, 
     }
 }
 
-// Block permutation: new position block pb holds old block src[pb] (w indices each).
 struct BjPerm {
   int src[8];
 };
+// dst = src, n*n doubles (an SM copy: inside the captured sweep body a memcpy node would go to a
+// copy engine shared by every chain)
+__global__ void k_bj_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 __global__ void k_bj_perm(const double* __restrict__ Gin, const double* __restrict__ Zin, int n, int w, BjPerm p,
                           double* __restrict__ Gout, double* __restrict__ Zout) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
@@ -109,9 +117,21 @@ __global__ void k_bj_perm(const double* __restrict__ Gin, const double* __restri
   Zout[i + (int64_t)j * n] = Zin[i + (int64_t)oj * n];          // Z: columns only
 }
 
-// max_{i<j} |g_ij| / sqrt|g_ii g_jj| over real indices (orig >= 0); flag = (max > tol)
-__global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ Gp, int n, const int* __restrict__ orig,
-                                                    double tol, int* __restrict__ flag) {
+// Block permutation: new position block pb holds old block src[pb] (w indices each).
+// Original index held at position i when position block i / w holds original block arr[i / w]
+// (-1 for padding).
+__device__ __forceinline__ int bj_orig(const BjPerm& arr, int i, int w, int b) {
+  const int o = arr.src[i / w] * w + i % w;
+  return o < b ? o : -1;
+}
+
+// One sweep's convergence test: max_{i<j} |g_ij| / sqrt|g_ii g_jj| over real indices, against tol.
+// Continues the sweep loop (DevLoop) while above tol and fewer than max_sweeps sweeps ran; a loop
+// that stops on the cap flags ctrl->nonfinite bit 2 (informational: the Rayleigh-Ritz rotation is
+// then exact but G not fully diagonal, so the residual test of l. 7 simply locks less).
+__global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ Gp, int n, BjPerm arr, int w, int b,
+                                                    double tol, int* __restrict__ counter, int max_sweeps,
+                                                    Ctrl* ctrl, DevLoop loop) {
   double mx = 0.0, dmax = 0.0;
   for (int i = threadIdx.x; i < n; i += 1024) dmax = fmax(dmax, fabs(Gp[i + (int64_t)i * n]));
   __shared__ double red[32];
@@ -129,7 +149,7 @@ __global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ G
   __syncthreads();
   for (int64_t idx = threadIdx.x; idx < (int64_t)n * n; idx += 1024) {
     const int i = (int)(idx % n), j = (int)(idx / n);
-    if (i >= j || orig[i] < 0 || orig[j] < 0) continue;
+    if (i >= j || bj_orig(arr, i, w, b) < 0 || bj_orig(arr, j, w, b) < 0) continue;
     const double g = fabs(Gp[idx]);
     if (g > gfloor) mx = fmax(mx, g / fmax(sqrt(fabs(Gp[i + (int64_t)i * n] * Gp[j + (int64_t)j * n])), 1e-300));
   }
@@ -139,24 +159,30 @@ __global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ G
   if (threadIdx.x == 0) {
     double v = 0.0;
     for (int k = 0; k < 32; ++k) v = fmax(v, red[k]);
-    *flag = v > tol ? 1 : 0;
+    const int cnt = ++(*counter);
+    const bool above = v > tol;
+    if (ctrl) ctrl->pad[0] += 1;                   // cumulative sweeps (stats)
+    if (above && cnt >= max_sweeps && ctrl) atomicOr(&ctrl->nonfinite, 2);
+    dev_loop_continue(loop, above && cnt < max_sweeps);
   }
 }
 
 // theta ascending over the real indices, Zout[:, rank] = Zp[orig rows, position] (b x b, ld b)
 __global__ void __launch_bounds__(512) k_bj_final(const double* __restrict__ Gp, const double* __restrict__ Zp, int n,
-                                                  const int* __restrict__ orig, int b, double* __restrict__ theta,
+                                                  BjPerm arr, int w, int b, double* __restrict__ theta,
                                                   double* __restrict__ Zout) {
   __shared__ int rank_s[512];
   for (int pos = threadIdx.x; pos < n; pos += 512) {
     int rk = -1;
-    if (orig[pos] >= 0) {
+    const int op = bj_orig(arr, pos, w, b);
+    if (op >= 0) {
       const double v = Gp[pos + (int64_t)pos * n];
       rk = 0;
       for (int q = 0; q < n; ++q) {
-        if (orig[q] < 0) continue;
+        const int oq = bj_orig(arr, q, w, b);
+        if (oq < 0) continue;
         const double u = Gp[q + (int64_t)q * n];
-        rk += (u < v) || (u == v && orig[q] < orig[pos]);
+        rk += (u < v) || (u == v && oq < op);
       }
       theta[rk] = v;
     }
@@ -172,8 +198,6 @@ __global__ void __launch_bounds__(512) k_bj_final(const double* __restrict__ Gp,
   }
 }
 
-__global__ void k_bj_flag(Ctrl* ctrl) { atomicOr(&ctrl->nonfinite, 2); }
-
 size_t blockjac_scratch_doubles(int b) {
   const int nb = 2 * ((b + 127) / 128), w = (b + nb - 1) / nb, n = nb * w;
   return (size_t)4 * n * n + (size_t)(nb / 2) * 128 * 128 + (size_t)n + 4096;
@@ -181,6 +205,12 @@ size_t blockjac_scratch_doubles(int b) {
 
 // G (b x b, upper, ldg) = Z diag(theta) Z^T, theta ascending (b), Z (b x b, ld b).
 // scratch: blockjac_scratch_doubles(b) doubles; jscratch: the batched one-CTA Jacobi scratch.
+//
+// The round-robin schedule is fixed, so the host computes every round's block permutation
+// up front; the blocks are first arranged as in the last round of a sweep, which makes all
+// sweeps identical.  The sweeps run as a device-decided loop (device_while): inside a
+// CUDA-graph capture a WHILE conditional node, so a b > 128 outer iteration replays from
+// one graph with no host synchronisation.
 int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* jscratch, double* theta,
                   double* Zout, Ctrl* ctrl, cudaStream_t s) {
   const int nb = 2 * ((b + 127) / 128), P = nb / 2;
@@ -195,89 +225,105 @@ int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* 
   double* T2 = T + (size_t)n * n;
   double* Q = T2 + (size_t)n * n;
   double* th = Q + (size_t)P * 128 * 128;
-  int* orig_d = reinterpret_cast<int*>(th + n);
-  int* flag_d = orig_d + 512;
-  int* flag_h = nullptr;
+  int* aux_d = reinterpret_cast<int*>(th + n);      // [0] loop flag, [1] sweep counter
+  int* flag_d = aux_d;
+  int* counter_d = aux_d + 1;
   static thread_local int* t_flag = nullptr;
-  static thread_local cudaEvent_t t_ev = nullptr;
-  if (!t_flag) {
-    SCSF_CUDA_CHECK(cudaMallocHost(&t_flag, sizeof(int)));
-    SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&t_ev, cudaEventBlockingSync | cudaEventDisableTiming));
-  }
-  flag_h = t_flag;
+  if (!t_flag) SCSF_CUDA_CHECK(cudaMallocHost(&t_flag, sizeof(int)));
   const size_t smm = (size_t)(m * (BJ_R + 1) + m * m) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_bj_blkmm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((128 * (BJ_R + 1) + 128 * 128) * sizeof(double))));
-    attr = true;
-  }
-  double* bound_d = reinterpret_cast<double*>(flag_d + 16);
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(k_bj_blkmm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)((128 * (BJ_R + 1) + 128 * 128) * sizeof(double)));
+  });
+  SCSF_CUDA_CHECK(attr_err);
+  double* bound_d = reinterpret_cast<double*>(aux_d + 16);
   k_bj_bound<<<1, 512, 0, s>>>(G, ldg, b, bound_d);
   SCSF_LAUNCH_CHECK();
-  k_bj_load<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(G, ldg, b, n, bound_d, Gp, Zp);
+  k_bj_load<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(G, ldg, b, n, bound_d, Gp, Zp, counter_d);
   SCSF_LAUNCH_CHECK();
-  // tournament (circle method): c[0] fixed, c[1..nb-1] rotate; pairs (c[i], c[nb-1-i]) -> positions (2i, 2i+1)
-  std::vector<int> c(nb), arr(nb), cur(nb);
-  for (int i = 0; i < nb; ++i) c[i] = i, cur[i] = i;
-  std::vector<int> orig(n);
-  for (int i = 0; i < n; ++i) orig[i] = (i < b) ? i : -1;
-  const int max_sweeps = 30;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    for (int r = 0; r < nb - 1; ++r) {
-      for (int i = 0; i < P; ++i) {
-        arr[2 * i] = c[i];
-        arr[2 * i + 1] = c[nb - 1 - i];
-      }
-      // bring the arrangement `arr` into place: new position pb holds the block now at position of arr[pb]
-      BjPerm pm{};
-      bool ident = true;
-      for (int pb = 0; pb < nb; ++pb) {
-        int at = 0;
-        while (cur[at] != arr[pb]) ++at;
-        pm.src[pb] = at;
-        ident = ident && (at == pb);
-      }
-      if (!ident) {
-        k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(Gp, Zp, n, w, pm, T, T2);
-        SCSF_LAUNCH_CHECK();
-        std::swap(Gp, T);
-        std::swap(Zp, T2);
-        std::vector<int> no(n);
-        for (int i = 0; i < n; ++i) no[i] = orig[pm.src[i / w] * w + i % w];
-        orig.swap(no);
-        cur = arr;
-      }
-      // P sub-problems on the diagonal blocks of width m, one CTA each
-      SCSF_TRY(jacobi_batched_impl(Gp, n, m, P, (int64_t)m * (n + 1), jscratch, th, Q, ctrl, s));
-      // G <- Q^T G Q  (T = G Q, G = T^T Q by symmetry),  Z <- Z Q
-      k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, s>>>(Gp, n, 0, Q, m, T);
-      SCSF_LAUNCH_CHECK();
-      k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, s>>>(T, n, 1, Q, m, Gp);
-      SCSF_LAUNCH_CHECK();
-      k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, s>>>(Zp, n, 0, Q, m, T);
-      SCSF_LAUNCH_CHECK();
-      std::swap(Zp, T);
-      // rotate the circle
-      const int last = c[nb - 1];
-      for (int i = nb - 1; i > 1; --i) c[i] = c[i - 1];
-      c[1] = last;
+  // tournament (circle method): c[0] fixed, c[1..nb-1] rotate; pairs (c[i], c[nb-1-i]) -> positions (2i, 2i+1).
+  // After nb - 1 rounds the circle is back where it started, so every sweep has the same arrangements.
+  std::vector<BjPerm> arr(nb - 1);
+  std::vector<int> c(nb);
+  for (int i = 0; i < nb; ++i) c[i] = i;
+  for (int r = 0; r < nb - 1; ++r) {
+    for (int i = 0; i < P; ++i) {
+      arr[r].src[2 * i] = c[i];
+      arr[r].src[2 * i + 1] = c[nb - 1 - i];
     }
-    SCSF_CUDA_CHECK(cudaMemcpyAsync(orig_d, orig.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
-    k_bj_offmax<<<1, 1024, 0, s>>>(Gp, n, orig_d, 1e-14, flag_d);
-    SCSF_LAUNCH_CHECK();
-    SCSF_CUDA_CHECK(cudaMemcpyAsync(flag_h, flag_d, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SCSF_CUDA_CHECK(cudaEventRecord(t_ev, s));
-    SCSF_CUDA_CHECK(cudaEventSynchronize(t_ev));
-    if (*flag_h == 0) break;
+    const int last = c[nb - 1];
+    for (int i = nb - 1; i > 1; --i) c[i] = c[i - 1];
+    c[1] = last;
   }
-  if (sweep >= max_sweeps && ctrl) {
-    k_bj_flag<<<1, 1, 0, s>>>(ctrl);
+  // permutation taking arrangement `from` (position -> original block) to `to`
+  auto perm_between = [&](const BjPerm& from, const BjPerm& to, BjPerm& pm) {
+    bool ident = true;
+    for (int pb = 0; pb < nb; ++pb) {
+      int at = 0;
+      while (from.src[at] != to.src[pb]) ++at;
+      pm.src[pb] = at;
+      ident = ident && (at == pb);
+    }
+    return ident;
+  };
+  BjPerm idn{};
+  for (int i = 0; i < nb; ++i) idn.src[i] = i;
+  const BjPerm& A_last = arr[nb - 2];
+  // bring the identity arrangement into the last round's (the loop's invariant at each sweep start)
+  BjPerm pm0;
+  if (!perm_between(idn, A_last, pm0)) {
+    k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(Gp, Zp, n, w, pm0, T, T2);
+    SCSF_LAUNCH_CHECK();
+    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T, Gp, (int64_t)n * n);
+    SCSF_LAUNCH_CHECK();
+    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T2, Zp, (int64_t)n * n);
     SCSF_LAUNCH_CHECK();
   }
-  SCSF_CUDA_CHECK(cudaMemcpyAsync(orig_d, orig.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
-  k_bj_final<<<1, 512, 0, s>>>(Gp, Zp, n, orig_d, b, theta, Zout);
+  std::vector<BjPerm> pms(nb - 1);
+  std::vector<bool> ident(nb - 1);
+  for (int r = 0; r < nb - 1; ++r) ident[r] = perm_between(r == 0 ? A_last : arr[r - 1], arr[r], pms[r]);
+  const int max_sweeps = 30;
+  // One sweep.  Every round ends with G and Z back in (Gp, Zp): a permutation or Z <- Z Q that
+  // lands in T / T2 is copied back, so the captured body is position-independent.
+  auto sweep = [&](cudaStream_t bs, const DevLoop& loop) -> int {
+    for (int r = 0; r < nb - 1; ++r) {
+      if (!ident[r]) {
+        k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, bs>>>(Gp, Zp, n, w, pms[r], T, T2);
+        SCSF_LAUNCH_CHECK();
+      }
+      const double* Gr = ident[r] ? Gp : T;
+      const double* Zr = ident[r] ? Zp : T2;
+      // P sub-problems on the diagonal blocks of width m, one CTA each
+      SCSF_TRY(jacobi_batched_impl(Gr, n, m, P, (int64_t)m * (n + 1), jscratch, th, Q, ctrl, bs));
+      // G <- Q^T G Q  (X = G Q, G = X^T Q by symmetry),  Z <- Z Q
+      if (!ident[r]) {                                   // G' in T, Z' in T2; Gp, Zp are free
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gr, n, 0, Q, m, Gp);     // Gp = (T) Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 1, Q, m, T);      // T = Gp^T Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zr, n, 0, Q, m, Zp);     // Zp = T2 Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T, Gp, (int64_t)n * n);
+        SCSF_LAUNCH_CHECK();
+      } else {
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 0, Q, m, T);      // T = Gp Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(T, n, 1, Q, m, Gp);      // Gp = T^T Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zp, n, 0, Q, m, T2);     // T2 = Zp Q
+        SCSF_LAUNCH_CHECK();
+        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T2, Zp, (int64_t)n * n);
+        SCSF_LAUNCH_CHECK();
+      }
+    }
+    k_bj_offmax<<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, max_sweeps, ctrl, loop);
+    SCSF_LAUNCH_CHECK();
+    return SCSF_OK;
+  };
+  SCSF_TRY(device_while(s, flag_d, t_flag, max_sweeps, sweep));
+  k_bj_final<<<1, 512, 0, s>>>(Gp, Zp, n, A_last, w, b, theta, Zout);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

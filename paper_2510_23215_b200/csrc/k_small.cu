@@ -660,8 +660,9 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
   // SURVEY f2 (Alg. 1 l. 5's staggered update, ChASE-style): per-column degree for the next
   // filter.  A column with relative residual r and scaled Ritz value t = (theta - c)/e gains a
   // factor g = |t| + sqrt(t^2 - 1) per degree over the damped interval, so reaching
-  // 0.1 tol takes ceil(ln(10 r / tol) / ln g) steps; clamped to [4, m] and made non-decreasing
-  // in the column index (Ritz order).  deg == NULL: uniform degree m (reading R8).
+  // 0.1 tol takes ceil(ln(10 r / tol) / ln g) steps; clamped to [4, m], rounded up to = m mod 3
+  // and made non-decreasing in the column index (Ritz order).  deg == NULL: uniform degree m
+  // (reading R8).
   if (deg) {
     __syncwarp();
     const int kLn = ctrl->kL;
@@ -675,7 +676,10 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
         if (t > 1.0 && isfinite(r)) {
           const double g = t + sqrt((t - 1.0) * (t + 1.0));
           const double need = log(fmax(10.0 * r / tol, 1.0)) / log(g);
-          mj = (int)fmin((double)mdeg, fmax(4.0, ceil(need)));
+          const int nd = (int)fmin((double)mdeg, fmax(4.0, ceil(need)));
+          // round up to nd = m (mod 3): the streaming filter rotates three buffers, so a column
+          // that stops after nd steps then holds its Y_nd in the same buffer as Y_m
+          mj = mdeg - 3 * ((mdeg - nd) / 3);
         }
       }
       // running maximum across the columns (lane order, then chunk order)

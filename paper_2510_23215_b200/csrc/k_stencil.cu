@@ -14,6 +14,9 @@
 // and stay L2-resident.
 #include "common.cuh"
 
+#include <atomic>
+#include <mutex>
+
 #include <cooperative_groups.h>
 
 namespace scsf {
@@ -373,14 +376,19 @@ template <int DIM, int CB>
 __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
     const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n,
     const double* __restrict__ X, const double* Xp, double* Out,   // Out may alias Xp (same-index RMW)
-    int64_t ldv, int ncols, const double* __restrict__ fp, int step) {
+    int64_t ldv, int ncols, const double* __restrict__ fp, int step, const int* __restrict__ deg) {
   const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
   if (k0 >= ldv) return;
   double a, b, c;
   step_scalars(fp, step, a, b, c);
   const int64_t sxy = (int64_t)nx * ny;
-  const int j0 = blockIdx.y * CB;
+  int j0 = blockIdx.y * CB;
   const int j1 = min(ncols, j0 + CB);
+  // SURVEY f2 (Alg. 1 l. 5's staggered update): a column whose degree deg[j] <= step is finished
+  // and left untouched; degrees are non-decreasing in j, so the finished ones are a prefix
+  if (deg)
+    while (j0 < j1 && __ldg(deg + j0) <= step) ++j0;
+  if (j0 >= j1) return;
   if (k0 + 4 <= n) {
     const double4 dg = ldg4_nc(cf + k0);
     const double4 cxp = ldg4_nc(cf + ldc + k0);
@@ -1021,6 +1029,11 @@ __global__ void k_resid_sum(const double* __restrict__ P, int nblk, double* __re
 
 // Residual norms from V without materialising W = A V (flux stencils, nx % 4 == 0, no row
 // partition); returns false when the caller must use stencil_impl + resid_impl instead.
+// doubles of P that k_stencil_resid writes for ncols columns of ld ldv (2 partial sums per CTA)
+size_t resid_partial_doubles(int64_t ldv, int ncols) {
+  return (size_t)2 * ncols * ceil_div(ceil_div(ldv, 4), SV_THREADS);
+}
+
 int stencil_resid_impl(const scsf_ops* ops, int op, const double* V, int64_t ldv, int ncols, const double* theta,
                        double* res, double* wn, double* P, cudaStream_t s, bool* done) {
   *done = false;
@@ -1221,29 +1234,29 @@ __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, 
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
                             const int* __restrict__ deg);
 // Can this device co-schedule a 16-CTA cluster of the largest filter CTA (768 threads, 200 KB)?
-// Checked once; a device that cannot (fewer SMs per GPC, partitioned GPUs) keeps clusters <= 8.
+// Probed once inside stencil_init_attrs() (std::call_once, before any chain thread launches);
+// a device that cannot (fewer SMs per GPC, partitioned GPUs) keeps clusters <= 8.
+static std::atomic<int> g_cs16{-1};
+static int probe_cs16() {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16, 1, 1);
+  cfg.blockDim = dim3(CL_T, 1, 1);
+  cfg.dynamicSmemBytes = 200 * 1024;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, k_filter_cl<16, 4>, &cfg) == cudaSuccess && nclusters > 0;
+  cudaGetLastError();
+  return ok ? 1 : 0;
+}
 static bool cs16_ok() {
-  static int v = -1;
-  if (v < 0) {
-    v = 0;
-    if (stencil_init_attrs() == SCSF_OK) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(16, 1, 1);
-      cfg.blockDim = dim3(CL_T, 1, 1);
-      cfg.dynamicSmemBytes = 200 * 1024;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 16;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, k_filter_cl<16, 4>, &cfg) == cudaSuccess && nclusters > 0) v = 1;
-      cudaGetLastError();
-    }
-  }
-  return v == 1;
+  if (g_cs16.load(std::memory_order_acquire) < 0 && stencil_init_attrs() != SCSF_OK) return false;
+  return g_cs16.load(std::memory_order_acquire) == 1;
 }
 
 static int cluster_size_for(const scsf_ops* ops) {
@@ -1335,9 +1348,7 @@ static cudaError_t launch_cl(cudaLaunchConfig_t& cfg, int cs, int cb, const doub
 
 // All dynamic-shared-memory opt-ins of the filter kernels, set once before any
 // launch (in particular before a CUDA-graph capture).
-int stencil_init_attrs() {
-  static bool done = false;
-  if (done) return SCSF_OK;
+static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * RES_MAX_N * (int)sizeof(double)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_stencil_vib_t, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1357,9 +1368,16 @@ int stencil_init_attrs() {
   SCSF_RP_ATTR(1); SCSF_RP_ATTR(2); SCSF_RP_ATTR(4); SCSF_RP_ATTR(8);
 #undef SCSF_RP_ATTR
   g_res_attr = 1;
-  done = true;
+  g_cs16.store(probe_cs16(), std::memory_order_release);     // published once, after the opt-ins
   return SCSF_OK;
 }
+int stencil_init_attrs() {
+  static std::once_flag once;
+  static int status = SCSF_OK;
+  std::call_once(once, [] { status = stencil_init_attrs_once(); });
+  return status;
+}
+
 
 // Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
@@ -1414,8 +1432,14 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
 }
 
 // Out[:, 0:ncols] = step-th filter update (or A X when step < 0).
+// Does stencil_impl dispatch the vectorised k_stencil_v4 (the one streaming kernel that honours
+// per-column degrees) for these operators and blocks?
+bool stencil_v4_ok(const scsf_ops* ops, int64_t ldv) {
+  return ops->stencil == SCSF_STENCIL_FLUX && ops->nx % 4 == 0 && ldv % 4 == 0 && ops->ld % 4 == 0;
+}
+
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out,
-                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s) {
+                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s, const int* deg) {
   if (ncols <= 0) return SCSF_OK;
   int64_t n = (int64_t)ops->nx * ops->ny * ops->nz;
   const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
@@ -1441,10 +1465,16 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
     constexpr int CB = 4;
     dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
     if (ops->dim == 2)
-      k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+      k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step,
+                                                   deg);
     else
-      k_stencil_v4<3, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);
+      k_stencil_v4<3, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step,
+                                                   deg);
   } else {
+    if (deg) {
+      set_error("per-column filter degrees need the vectorised stencil (nx %% 4 == 0, aligned blocks)");
+      return SCSF_ERR_ARG;
+    }
     dim3 g(ceil_div(n, ST_THREADS), ceil_div(ncols, ST_COLS));
     if (ops->dim == 2)
       k_stencil<2><<<g, ST_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step);

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -27,7 +28,8 @@ namespace scsf {
 
 // kernels (k_*.cu)
 int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp, double* Out,
-                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s);
+                 int64_t ldv, int ncols, const double* fp, int step, cudaStream_t s, const int* deg = nullptr);
+bool stencil_v4_ok(const scsf_ops* ops, int64_t ldv);
 bool filter_resident_ok(const scsf_ops* ops);
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
                          const double* fp, int m, cudaStream_t s, const int* deg = nullptr);
@@ -43,6 +45,7 @@ int gemm_nn(const double* X, int64_t ldx, int64_t n, int b1, const double* M, in
 int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M, int64_t ldm, int b2,
                double alpha, double beta, double* Out, int64_t ldo, int tri, cudaStream_t s);
 size_t tn_partial_doubles(int64_t n, int b1, int b2);
+size_t resid_partial_doubles(int64_t ldv, int ncols);
 int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y2, int64_t ldy, int b, int64_t n,
                  double* C, int64_t ldc, double* P, cudaStream_t s);
 int symm_upper_impl(double* A, int b, int64_t ld, cudaStream_t s);
@@ -101,7 +104,8 @@ static void carve(Arena& a, SolveWS& w, const scsf_ops* ops, int b, const DistCt
   w.C2 = a.take<double>(2 * bb);
   w.Tb = a.take<double>(bb);
   w.Mb = a.take<double>(bb);
-  w.P = a.take<double>((int64_t)tn_partial_doubles(n, b, b));
+  // split-K partials of the TN products, and the fused residual pass's per-CTA partials
+  w.P = a.take<double>((int64_t)std::max(tn_partial_doubles(n, b, b), resid_partial_doubles(w.ldv, b)));
   w.theta = a.take<double>(b);
   w.theta_sorted = a.take<double>(b);
   w.res = a.take<double>(b);
@@ -142,19 +146,68 @@ int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_byte
   return SCSF_OK;
 }
 
+// ---- optional DGEMM timers (scsf_set_timing): CUDA events around every tall-skinny DGEMM
+// tile launch of an iteration, summed after the iteration's control-block read; the flops are
+// the algorithmic ones of the product (upper-triangle Grams count their unique entries)
+static int g_timing = 0;
+struct GemmTiming {
+  std::vector<cudaEvent_t> ev;     // pairs (begin, end), reused
+  std::vector<double> flops;
+  size_t used = 0;
+  double ms = 0.0, total_flops = 0.0;
+};
+static thread_local GemmTiming* t_gt = nullptr;
+static int gt_begin(cudaStream_t s) {
+  GemmTiming* g = t_gt;
+  if (!g) return SCSF_OK;
+  if (g->used + 2 > g->ev.size()) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEvent_t e;
+      SCSF_CUDA_CHECK(cudaEventCreate(&e));
+      g->ev.push_back(e);
+    }
+  }
+  SCSF_CUDA_CHECK(cudaEventRecord(g->ev[g->used], s));
+  return SCSF_OK;
+}
+static int gt_end(cudaStream_t s, double flops) {
+  GemmTiming* g = t_gt;
+  if (!g) return SCSF_OK;
+  SCSF_CUDA_CHECK(cudaEventRecord(g->ev[g->used + 1], s));
+  if (g->flops.size() < g->ev.size() / 2) g->flops.resize(g->ev.size() / 2);
+  g->flops[g->used / 2] = flops;
+  g->used += 2;
+  return SCSF_OK;
+}
+// after a synchronisation that follows every recorded pair
+static int gt_collect() {
+  GemmTiming* g = t_gt;
+  if (!g) return SCSF_OK;
+  for (size_t i = 0; i < g->used; i += 2) {
+    float ms = 0.f;
+    SCSF_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev[i], g->ev[i + 1]));
+    g->ms += ms;
+    g->total_flops += g->flops[i / 2];
+  }
+  g->used = 0;
+  return SCSF_OK;
+}
+
 // ---- the exchange points of the row-partitioned solve (no-ops on one GPU) ----
 // C = X^T Y summed over ranks (Gram / projection blocks, Alg. 3 ll. 4-5)
 static int gram(SolveWS& w, const double* X, int b1, const double* Y, int b2, int sym, double* C,
                 cudaStream_t s) {
+  SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_tn(X, w.ldv, b1, Y, w.ldv, b2, w.n, 1.0, sym, C, b1, w.P, s));
+  SCSF_TRY(gt_end(s, sym ? (double)w.n * b1 * (b1 + 1) : 2.0 * w.n * b1 * b2));
   if (w.comm) SCSF_TRY(w.comm->allreduce_sum(C, (size_t)b1 * b2, s));
   return SCSF_OK;
 }
 
 // One stencil application (filter step `step`, or A X when step < 0) on ncols columns.
 static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const double* Xp, double* Out, int ncols,
-                int step, cudaStream_t s) {
-  if (!w.comm) return stencil_impl(ops, op, X, Xp, Out, w.ldv, ncols, w.fp, step, s);
+                int step, cudaStream_t s, const int* deg = nullptr) {
+  if (!w.comm) return stencil_impl(ops, op, X, Xp, Out, w.ldv, ncols, w.fp, step, s, deg);
   SCSF_TRY(pack_rows_impl(X, w.ldv, w.n, w.nx, ncols, w.send_lo, w.send_hi, s));
   SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
   return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, w.comm->rank > 0 ? w.recv_lo : nullptr,
@@ -165,7 +218,9 @@ static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const 
 static int cholqr_pass(SolveWS& w, double* Y, double* Out, int ncols, cudaStream_t s) {
   SCSF_TRY(gram(w, Y, ncols, Y, ncols, 1, w.S, s));
   SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n_glob, w.Rinv, w.Gwork, w.ctrl, s));
+  SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn_ex(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, 1, s));
+  SCSF_TRY(gt_end(s, (double)w.n * ncols * (ncols + 1)));                     // triangular R^{-1}
   return SCSF_OK;
 }
 
@@ -180,8 +235,10 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
   spmm_cols += ba;
   SCSF_TRY(gram(w, Va, ba, Wa, ba, 1, w.S, s));
   SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
+  SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Va, w.ldv, s));
   SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
+  SCSF_TRY(gt_end(s, 4.0 * w.n * ba * ba));
   SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
   if (w.comm) {
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
@@ -214,7 +271,9 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   double* Va = w.V + (int64_t)k0 * w.ldv;
   double* Wa = w.W + (int64_t)k0 * w.ldv;
   SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
+  SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_tn_dual(Va, w.ldv, Va, Wa, w.ldv, ba, w.n, w.C2, ba, w.P, s));
+  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * (ba + 1)));                               // two upper Grams
   if (w.comm) SCSF_TRY(w.comm->allreduce_sum(w.C2, (size_t)2 * bb, s));
   const double* S2 = w.C2;
   double* H = w.C2 + bb;
@@ -224,7 +283,9 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(gemm_tn(w.Rinv, ba, ba, w.Tb, ba, ba, ba, 1.0, 1, w.S, ba, w.P, s));           // G = R2^{-T} T (upper)
   SCSF_TRY(jacobi_impl(w.S, ba, ba, w.Gwork, w.Zwork, w.theta + k0, w.Zs, w.ctrl, s));
   SCSF_TRY(gemm_nn_ex(w.Rinv, ba, ba, ba, w.Zs, ba, ba, 1.0, 0.0, w.Mb, ba, 0, s));        // M = R2^{-1} Z
+  SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Va, w.ldv, s));
+  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * ba));
   // residuals of A V by one stencil pass (cheaper than the n x b x b product W1 M); without a row
   // partition the pass is fused with the norms and W is not written (only the residuals use it)
   bool fused = false;
@@ -254,19 +315,9 @@ static bool inherit_bounds() {
   return v == 1;
 }
 
-// per-column filter degree (SCSF_ADAPTIVE_DEGREE=1; default: uniform degree, R8)
-static bool adaptive_degree() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SCSF_ADAPTIVE_DEGREE");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
 int fill_int_impl(int* p, int n, int v, cudaStream_t s);
 
 // ---- optional phase timers (scsf_set_timing) ----
-static int g_timing = 0;
 int set_timing(int on) {
   int old = g_timing;
   g_timing = on ? 1 : 0;
@@ -335,10 +386,11 @@ static int clear_chol_flag(SolveWS& w, cudaStream_t s) {
 // SCSF_GRAPHS=0, under SCSF_DEBUG_SYNC=1 and for the row-partitioned solve
 // (its loopback collectives synchronise on the host).
 struct GraphKey {
-  const void* V;
-  const void* coef;
+  // every device pointer an iteration's launches capture, and every shape / kernel choice:
+  // a cached graph is replayed only on the exact buffers and operator kind it was captured for
+  const void *V, *W, *T1, *T2, *P, *ctrl, *fp, *coef;
   int64_t n, ldv, ld, dims;
-  int b, kL, degree, L, timing;
+  int b, kL, degree, L, timing, stencil, ncoef, deg_on;
   double tol;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
@@ -350,12 +402,19 @@ struct GraphKeyHash {
     return h;
   }
 };
-struct GraphEntry {
+// The exec is destroyed when the last holder lets go: the cache on eviction, or a thread that
+// looked it up just before the eviction, after its cudaGraphLaunch (an in-flight executable
+// graph is freed asynchronously on completion).
+struct GraphExec {
   cudaGraphExec_t exec = nullptr;
   int kernels = 0;
+  ~GraphExec() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
 };
 static std::mutex g_graph_mu;
-static std::unordered_map<GraphKey, GraphEntry, GraphKeyHash>* g_graphs = nullptr;
+static std::unordered_map<GraphKey, std::shared_ptr<GraphExec>, GraphKeyHash>* g_graphs = nullptr;
+constexpr size_t GRAPH_CACHE_MAX = 20000;
 
 static bool graphs_enabled() {
   static int v = -1;
@@ -367,22 +426,19 @@ static bool graphs_enabled() {
 }
 
 template <class F>
-static int graph_run(const GraphKey& key0, F&& body, cudaStream_t s) {
-  GraphKey key;
-  memset(&key, 0, sizeof(key));                        // padding bytes take part in the hash / compare
-  key.V = key0.V; key.coef = key0.coef; key.n = key0.n; key.ldv = key0.ldv; key.ld = key0.ld;
-  key.dims = key0.dims; key.b = key0.b; key.kL = key0.kL; key.degree = key0.degree; key.L = key0.L;
-  key.timing = key0.timing; key.tol = key0.tol;
-  GraphEntry e;
+static int graph_run(const GraphKey& key, F&& body, cudaStream_t s) {
+  std::shared_ptr<GraphExec> e;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    if (!g_graphs) g_graphs = new std::unordered_map<GraphKey, GraphEntry, GraphKeyHash>();
+    if (!g_graphs) g_graphs = new std::unordered_map<GraphKey, std::shared_ptr<GraphExec>, GraphKeyHash>();
     auto it = g_graphs->find(key);
     if (it != g_graphs->end()) e = it->second;
   }
-  if (!e.exec) {
+  if (!e) {
+    e = std::make_shared<GraphExec>();
     SCSF_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     set_capturing(true);
+    take_cond_kernels();
     const int r = body();
     set_capturing(false);
     cudaGraph_t g = nullptr;
@@ -401,26 +457,36 @@ static int graph_run(const GraphKey& key0, F&& body, cudaStream_t s) {
     if (nn) SCSF_CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
     for (auto nd : nodes) {
       cudaGraphNodeType t;
-      SCSF_CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
-      e.kernels += (t == cudaGraphNodeTypeKernel);
+      // (the runtime reports an error, not a type, for a conditional node: it is not a kernel)
+      if (cudaGraphNodeGetType(nd, &t) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      e->kernels += (t == cudaGraphNodeTypeKernel);
     }
-    SCSF_CUDA_CHECK(cudaGraphInstantiate(&e.exec, g, 0));
+    e->kernels += take_cond_kernels();                 // a conditional body counts once per replay
+    const cudaError_t ie = cudaGraphInstantiate(&e->exec, g, 0);
     cudaGraphDestroy(g);
+    SCSF_CUDA_CHECK(ie);
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    if (g_graphs->size() > 20000) g_graphs->clear();   // bound the cache (execs are leaked, not freed mid-use)
+    if (g_graphs->size() >= GRAPH_CACHE_MAX) g_graphs->clear();   // bound the cache; execs freed by their holders
     g_graphs->emplace(key, e);
   }
-  SCSF_CUDA_CHECK(cudaGraphLaunch(e.exec, s));
-  count_launch(e.kernels);
+  SCSF_CUDA_CHECK(cudaGraphLaunch(e->exec, s));
+  count_launch(e->kernels);
   return SCSF_OK;
 }
 
 // Solve operator `op`.  warm: V already holds the initial b-block (orthonormal).
 // On return w.V holds the final block sorted ascending with the sign convention,
 // w.theta_sorted the Ritz values.
-int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, double tol, int max_iter,
+int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg, double tol, int max_iter,
                bool warm, bool orthonormalize, uint64_t seed, SolveWS& w, scsf_stats* st, cudaStream_t s) {
   const int b = L + nex;
+  // degree_arg > 0: uniform degree m for every active column (reading R8); degree_arg < 0: per-column
+  // degrees (Alg. 1 l. 5's staggered update) chosen by k_lock, capped at |degree_arg|
+  const bool adaptive = degree_arg < 0;
+  const int degree = adaptive ? -degree_arg : degree_arg;
   const bool graphs = graphs_enabled() && !w.comm && s != nullptr && !g_timing;
   // With graphs, the operator's arrays are first copied into the chain's own
   // buffer, so every captured iteration is independent of the operator index.
@@ -441,11 +507,16 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   const double coef_bytes = 8.0 * ncoef(ops) * (double)w.n;
   PhaseTimer tm;
   SCSF_TRY(tm.init());
+  static thread_local GemmTiming t_gt_store;
+  t_gt_store.ms = 0.0;
+  t_gt_store.total_flops = 0.0;
+  t_gt_store.used = 0;
+  t_gt = tm.on ? &t_gt_store : nullptr;
   Ctrl h{};
   SCSF_TRY(gershgorin_impl(ops, op, w.gersh, s));
   SCSF_TRY(ctrl_init_impl(w.ctrl, w.gersh, s));
   w.mdeg = degree;
-  w.deg_on = (adaptive_degree() && !w.comm && filter_resident_ok(ops)) ? w.deg : nullptr;
+  w.deg_on = (adaptive && !w.comm && (filter_resident_ok(ops) || stencil_v4_ok(ops, w.ldv))) ? w.deg : nullptr;
   if (w.deg_on) SCSF_TRY(fill_int_impl(w.deg, b, degree, s));
   if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, w.goff, s));
   if (!warm || orthonormalize) {
@@ -478,9 +549,12 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
       F = y[1];
     } else {
       SCSF_TRY(step_table_impl(w.fp, degree, s));
-      SCSF_TRY(spmm(ops, op, w, y[0], nullptr, y[1], ba, 0, s));
+      // per-column degrees (f2): columns past their degree are skipped in place; k_lock rounds every
+      // degree to = m (mod 3), so each column's last output lands in y[m % 3] as well
+      const int* dg = w.deg_on ? w.deg_on + kLc : nullptr;
+      SCSF_TRY(spmm(ops, op, w, y[0], nullptr, y[1], ba, 0, s, dg));
       for (int st_i = 1; st_i < degree; ++st_i)
-        SCSF_TRY(spmm(ops, op, w, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], ba, st_i, s));
+        SCSF_TRY(spmm(ops, op, w, y[st_i % 3], y[(st_i - 1) % 3], y[(st_i + 1) % 3], ba, st_i, s, dg));
       F = y[degree % 3];
     }
     SCSF_TRY(tm.mark(1, s));
@@ -488,7 +562,9 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     if (kLc > 0) {
       for (int rep = 0; rep < 2; ++rep) {
         SCSF_TRY(gram(w, w.V, kLc, F, ba, 0, w.C, s));
+        SCSF_TRY(gt_begin(s));
         SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kLc, w.C, kLc, ba, -1.0, 1.0, F, w.ldv, s));
+        SCSF_TRY(gt_end(s, 2.0 * w.n * kLc * ba));
       }
     }
     // 3. CholQR, first pass (lands the block in V's active columns)
@@ -503,9 +579,16 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   while (kL < L && iters < max_iter && !(h.nonfinite & 1)) {
     ++iters;
     const int ba = b - kL;
-    if (graphs && ba <= 128) {          // b > 128: the block Jacobi synchronises per sweep (not capturable)
-      GraphKey key{};
+    if (graphs) {                       // b > 128: the block-Jacobi sweeps are a conditional WHILE node
+      GraphKey key;
+      memset(&key, 0, sizeof(key));                    // padding bytes take part in the hash / compare
       key.V = w.V;
+      key.W = w.W;
+      key.T1 = w.T1;
+      key.T2 = w.T2;
+      key.P = w.P;
+      key.ctrl = w.ctrl;
+      key.fp = w.fp;
       key.coef = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
       key.n = w.n;
       key.ldv = w.ldv;
@@ -515,6 +598,9 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
       key.degree = degree;
       key.L = L;
       key.timing = tm.on ? 1 : 0;
+      key.stencil = ops->stencil;
+      key.ncoef = ncoef(ops);
+      key.deg_on = w.deg_on ? 1 : 0;
       key.dims = ops->nx + 65536LL * (ops->ny + 65536LL * (ops->nz + 65536LL * ops->dim));
       key.tol = tol;
       SCSF_TRY(graph_run(key, [&]() { return iteration(kL); }, s));
@@ -530,6 +616,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     spmm_cols += colsteps + 2 * ba;
     SCSF_TRY(read_ctrl(w, h, s));
     SCSF_TRY(tm.accumulate());
+    SCSF_TRY(gt_collect());
     next_colsteps = h.pad[1];
     if (h.chol_fail) {
       // shifted CholQR was needed: one more CholQR pass, then redo the RR step
@@ -554,6 +641,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
   }
   std::swap(w.V, w.T1);
   SCSF_TRY(read_ctrl(w, h, s));
+  SCSF_TRY(gt_collect());
   int status = SCSF_OK;
   if (kL < L || (h.nonfinite & 1)) status = SCSF_ERR_NUMERICAL;
   if (st) {
@@ -571,6 +659,9 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree, do
     st->t_rr_ms = tm.rr;
     st->filter_bytes = filter_bytes;
     st->jacobi_sweeps = h.pad[0];
+    SCSF_TRY(gt_collect());
+    st->t_gemm_ms = t_gt ? t_gt->ms : 0.0;
+    st->gemm_flops = t_gt ? t_gt->total_flops : 0.0;
   }
   if (status != SCSF_OK)
     set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op,

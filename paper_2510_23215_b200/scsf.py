@@ -35,6 +35,9 @@ EXPORTED = [
 ]
 
 
+ABI_VERSION = 2                         # include/scsf.h SCSF_ABI_VERSION
+
+
 class ScsfError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"scsf {_STATUS.get(code, code)}: {msg}")
@@ -58,7 +61,8 @@ class scsf_stats(ctypes.Structure):
                 ("spmm_columns", ctypes.c_int64), ("max_rel_resid", ctypes.c_double),
                 ("beta", ctypes.c_double), ("t_filter_ms", ctypes.c_double), ("t_ortho_ms", ctypes.c_double),
                 ("t_rr_ms", ctypes.c_double), ("filter_bytes", ctypes.c_double),
-                ("jacobi_sweeps", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("jacobi_sweeps", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("t_gemm_ms", ctypes.c_double), ("gemm_flops", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -125,6 +129,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.scsf_abi_version() != ABI_VERSION:       # the ctypes structs below must match include/scsf.h
+        raise ImportError(f"libscsf.so ABI {lib.scsf_abi_version()} != binding ABI {ABI_VERSION}: rebuild")
     _lib = lib
     return lib
 
@@ -409,6 +415,12 @@ def solve_chains(ops: Operators, queue, n_chains: int, L: int, nex: int, degree:
     if raise_on_fail or code != SCSF_ERR_NUMERICAL:
         _check(code)
     return evals, (evecs if want_vecs else None), [stats[i].as_dict() for i in range(nq)]
+
+
+def chains_host_workspace_bytes(ops: Operators, L: int, nex: int) -> int:
+    """Per-chain workspace of scsf_solve_chains_host (bytes)."""
+    st = ops.c_struct()
+    return int(load_library().scsf_solve_chains_host_workspace_bytes(ctypes.byref(st), L, nex))
 
 
 def solve_chains_host(ops: Operators, queue, n_chains: int, L: int, nex: int, evals_host: torch.Tensor,

@@ -18,6 +18,12 @@ def device_problem(fields, device="cuda"):
     return ops, params
 
 
+# The paper metric ||Av - lam v|| / ||Av|| is what the solver locks on (<= tol); recomputed
+# here on the CPU it carries the rounding of A v - lam v (absolute ~eps ||A||, i.e. <= 1 % of
+# tol * lam_1 on C1-C5), so the re-check allows that much and no more.
+PAPER_TOL_SLACK = 1.1
+
+
 def check_pairs(fields, i, lam_gpu, V_gpu, L, ref=None, guard=8, ev_tol=1e-9, sine_tol=1e-6,
                 resid_tol=1e-8, orth_tol=1e-12, paper_tol=None):
     """Compare L GPU pairs of operator i with the oracle; returns a dict of measured errors."""
@@ -25,6 +31,8 @@ def check_pairs(fields, i, lam_gpu, V_gpu, L, ref=None, guard=8, ev_tol=1e-9, si
     normA = float(np.abs(A).sum(axis=1).max())
     if ref is None:
         ref = oeig.smallest_eigpairs(fields, i, L + guard)
+    # a reference is only truth if it converged (smallest_eigpairs raises otherwise; belt and braces)
+    assert np.all(ref.resid <= np.maximum(1e-12 * np.abs(ref.lam), 2e-14 * ref.normA)), ref.resid.max()
     lam = np.asarray(lam_gpu[:L])
     V = np.asarray(V_gpu[:, :L])
     ev, sine = checks.compare_pairs(ref.lam, ref.V, lam, V, L)

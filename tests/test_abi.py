@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_abi_version_and_binding_table(libpath):
     from paper_2510_23215_b200 import scsf
     lib = scsf.load_library(libpath)
-    assert lib.scsf_abi_version() == 1
+    assert lib.scsf_abi_version() == 2
     assert sorted(scsf.EXPORTED) == _declared()
     assert lib.scsf_launch_count() >= 0
 
@@ -97,3 +97,16 @@ def test_new_queries_and_argument_errors_without_gpu(libpath):
     bad_kind = scsf.scsf_ops(2, 8, 8, 1, 1, 5, 64, 1)
     assert lib.scsf_solve_workspace_bytes(ctypes.byref(bad_kind), 4, 1) >= 0
     assert lib.scsf_assemble_vibration(ctypes.byref(bad_kind), 0.1, 1, 1, 64, 1, None) == scsf.SCSF_ERR_ARG
+
+
+def test_library_has_no_undefined_internal_symbols():
+    """Every scsf:: function the library calls is defined in it (a declaration that drifted from
+    its definition would only fail at dlopen on the GPU box)."""
+    import shutil
+    import subprocess
+    from paper_2510_23215_b200 import build as b
+    nm = shutil.which("nm")
+    if nm is None or not os.path.exists(b.LIB):
+        pytest.skip("nm or libscsf.so missing")
+    out = subprocess.run([nm, "-D", "--undefined-only", b.LIB], capture_output=True, text=True).stdout
+    assert "scsf" not in out, [ln for ln in out.splitlines() if "scsf" in ln]

@@ -96,3 +96,29 @@ def test_clusters_and_subspace_sine():
     th = 1e-3
     V = np.array([[1, 0], [0, np.cos(th)], [0, np.sin(th)], [0, 0]])
     assert checks.subspace_sine(U, V) == pytest.approx(np.sin(th), rel=1e-9)
+
+
+@pytest.mark.parametrize("cfg_name,nx", [("C3", 12), ("C4", 6), ("C1", 10), ("V1", 8)])
+def test_inertia_counts_match_dense_eigvalsh(cfg_name, nx):
+    """O8's two counting routines (no-pivot banded LDL^T; block Schur complements + Haynsworth)
+    against counting the eigenvalues of the dense matrix (LAPACK via numpy) below each shift,
+    including shifts 1e-9 relative either side of an eigenvalue and between a close pair."""
+    cfg = synth.get_config(cfg_name).with_(nx=nx)
+    f = synth.make_batch(cfg, 1)
+    w = np.linalg.eigvalsh(op.assemble_dense(f, 0))
+    gaps = np.diff(w) / w[1:]
+    j = int(np.argmin(gaps[:40]))                      # closest pair among the low eigenvalues
+    shifts = [0.5 * w[0], w[3] * (1 - 1e-9), w[3] * (1 + 1e-9), w[10] * (1 - 1e-9), 0.5 * (w[j] + w[j + 1]),
+              0.5 * (w[25] + w[26]), 1.5 * w[-1]]
+    for sigma in shifts:
+        want = int(np.sum(w < sigma))
+        assert checks.inertia_blocks(f, 0, sigma) == want, sigma
+        if not getattr(f, "is_vib", False):
+            assert checks.inertia_below(f, 0, sigma) == want, sigma
+
+
+def test_smallest_eigpairs_raises_instead_of_returning_unconverged():
+    cfg = synth.get_config("C2").with_(nx=30, L=20)
+    f = synth.make_batch(cfg, 1)
+    with pytest.raises(eig.OracleNotConverged):
+        eig.smallest_eigpairs(f, 0, 20, max_dim=24)      # Krylov space capped far too small
