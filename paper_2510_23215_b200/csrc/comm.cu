@@ -80,6 +80,7 @@ NcclApi& nccl() {
 
 struct NcclComm final : Comm {
   ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
   ~NcclComm() override {
     if (comm) nccl().CommDestroy(comm);
   }

@@ -15,6 +15,9 @@ struct Comm {
   // send_lo -> rank-1 (lands in its recv_hi), send_hi -> rank+1 (lands in its recv_lo)
   virtual int halo(const double* send_lo, const double* send_hi, double* recv_lo, double* recv_hi, size_t count,
                    cudaStream_t s) = 0;
+  // stream-ordered without host participation (NCCL): the collectives may be captured into a
+  // CUDA graph; the loopback backend meets at host barriers and is not capturable
+  virtual bool capturable() const { return false; }
 };
 
 int comm_unique_id(void* id128);

@@ -13,13 +13,18 @@
 // |g_ij| <= 1e-14 sqrt|g_ii g_jj| (as the one-CTA Jacobi).
 #include "common.cuh"
 
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
 namespace scsf {
 
 int jacobi_batched_impl(const double* G, int64_t ldg, int bs, int batch, int64_t gstride, double* scratch,
-                        double* theta, double* Q, Ctrl* ctrl, cudaStream_t s);
+                        double* theta, double* Q, Ctrl* ctrl, cudaStream_t s, const int* skip);
+
+// Every kernel of a sweep takes `run` (the loop flag): inside a captured, unrolled sweep sequence
+// a sweep after convergence (*run == 0) returns at once.
+__device__ __forceinline__ bool bj_skip(const int* run) { return run && *(volatile const int*)run == 0; }
 
 // Gershgorin bound max_i sum_j |g_ij| of the upper-stored G (one CTA)
 __global__ void __launch_bounds__(512) k_bj_bound(const double* __restrict__ G, int64_t ldg, int b,
@@ -47,7 +52,10 @@ __global__ void __launch_bounds__(512) k_bj_bound(const double* __restrict__ G, 
 __global__ void k_bj_load(const double* __restrict__ G, int64_t ldg, int b, int n, const double* __restrict__ bound,
                           double* __restrict__ Gp, double* __restrict__ Zp, int* __restrict__ counter) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  if (i == 0 && j == 0) *counter = 0;                 // sweeps of this solve
+  if (i == 0 && j == 0) {
+    counter[0] = 0;                                   // sweeps of this solve
+    counter[-1] = 1;                                  // the loop flag: run the first sweep
+  }
   if (i >= n) return;
   double v = 0.0;
   if (i < b && j < b) v = (i <= j) ? G[i + (int64_t)j * ldg] : G[j + (int64_t)i * ldg];
@@ -60,7 +68,9 @@ __global__ void k_bj_load(const double* __restrict__ G, int64_t ldg, int b, int 
 // Q_q = Q + q m^2 (m x m, ld m).  CTA: 32 rows x the m columns of one block q.
 constexpr int BJ_R = 32;
 __global__ void __launch_bounds__(256) k_bj_blkmm(const double* __restrict__ X, int n, int transX,
-                                                  const double* __restrict__ Q, int m, double* __restrict__ Out) {
+                                                  const double* __restrict__ Q, int m, double* __restrict__ Out,
+                                                  const int* run) {
+  if (bj_skip(run)) return;
   extern __shared__ double sm[];
   double* xs = sm;                           // [m][BJ_R + 1]: xs[k][r]
   double* qs = sm + m * (BJ_R + 1);          // [m][m]: qs[k + c m]
@@ -103,13 +113,15 @@ struct BjPerm {
 };
 // dst = src, n*n doubles (an SM copy: inside the captured sweep body a memcpy node would go to a
 // copy engine shared by every chain)
-__global__ void k_bj_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t count) {
+__global__ void k_bj_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t count, const int* run) {
+  if (bj_skip(run)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
 
 __global__ void k_bj_perm(const double* __restrict__ Gin, const double* __restrict__ Zin, int n, int w, BjPerm p,
-                          double* __restrict__ Gout, double* __restrict__ Zout) {
+                          double* __restrict__ Gout, double* __restrict__ Zout, const int* run) {
+  if (bj_skip(run)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (i >= n) return;
   const int oi = p.src[i / w] * w + i % w, oj = p.src[j / w] * w + j % w;
@@ -132,6 +144,7 @@ __device__ __forceinline__ int bj_orig(const BjPerm& arr, int i, int w, int b) {
 __global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ Gp, int n, BjPerm arr, int w, int b,
                                                     double tol, int* __restrict__ counter, int max_sweeps,
                                                     Ctrl* ctrl, DevLoop loop) {
+  if (bj_skip(loop.flag)) return;                      // (unrolled sweeps after convergence)
   double mx = 0.0, dmax = 0.0;
   for (int i = threadIdx.x; i < n; i += 1024) dmax = fmax(dmax, fabs(Gp[i + (int64_t)i * n]));
   __shared__ double red[32];
@@ -196,6 +209,22 @@ __global__ void __launch_bounds__(512) k_bj_final(const double* __restrict__ Gp,
     if (rk < 0 || row >= b) continue;
     Zout[row + (int64_t)rk * b] = Zp[row + (int64_t)pos * n];
   }
+}
+
+// SCSF_BJ_UNROLL=k (default 8): inside a CUDA-graph capture, run k unrolled sweeps whose kernels
+// return at once after convergence; 0: a WHILE conditional node instead.  Measured on C3 (64
+// operators, 32 chains, m = 60, tools/graph_ab.py): unrolled 2.10-2.14 s, eager with a host
+// synchronisation per sweep 2.31 s, conditional node 2.57 s (device-launched bodies of the 32
+// chains' graphs do not overlap as well); 8 sweeps never truncated a solve there (3.26 sweeps
+// per iteration on average, identical to the unbounded loop)
+static int bj_unroll() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_BJ_UNROLL");
+    v = e ? atoi(e) : 8;
+    if (v < 0) v = 0;
+  }
+  return v;
 }
 
 size_t blockjac_scratch_doubles(int b) {
@@ -274,11 +303,11 @@ int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* 
   // bring the identity arrangement into the last round's (the loop's invariant at each sweep start)
   BjPerm pm0;
   if (!perm_between(idn, A_last, pm0)) {
-    k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(Gp, Zp, n, w, pm0, T, T2);
+    k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, s>>>(Gp, Zp, n, w, pm0, T, T2, nullptr);
     SCSF_LAUNCH_CHECK();
-    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T, Gp, (int64_t)n * n);
+    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T, Gp, (int64_t)n * n, nullptr);
     SCSF_LAUNCH_CHECK();
-    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T2, Zp, (int64_t)n * n);
+    k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, s>>>(T2, Zp, (int64_t)n * n, nullptr);
     SCSF_LAUNCH_CHECK();
   }
   std::vector<BjPerm> pms(nb - 1);
@@ -287,42 +316,52 @@ int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* 
   const int max_sweeps = 30;
   // One sweep.  Every round ends with G and Z back in (Gp, Zp): a permutation or Z <- Z Q that
   // lands in T / T2 is copied back, so the captured body is position-independent.
+  // unrolled mode (captured): a fixed number of sweeps whose kernels return at once after convergence
+  const int unroll = stream_capturing(s) ? bj_unroll() : 0;
+  const int cap = unroll > 0 ? unroll : max_sweeps;
   auto sweep = [&](cudaStream_t bs, const DevLoop& loop) -> int {
+    const int* run = loop.flag;
     for (int r = 0; r < nb - 1; ++r) {
       if (!ident[r]) {
-        k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, bs>>>(Gp, Zp, n, w, pms[r], T, T2);
+        k_bj_perm<<<dim3(ceil_div(n, 128), n), 128, 0, bs>>>(Gp, Zp, n, w, pms[r], T, T2, run);
         SCSF_LAUNCH_CHECK();
       }
       const double* Gr = ident[r] ? Gp : T;
       const double* Zr = ident[r] ? Zp : T2;
       // P sub-problems on the diagonal blocks of width m, one CTA each
-      SCSF_TRY(jacobi_batched_impl(Gr, n, m, P, (int64_t)m * (n + 1), jscratch, th, Q, ctrl, bs));
+      SCSF_TRY(jacobi_batched_impl(Gr, n, m, P, (int64_t)m * (n + 1), jscratch, th, Q, ctrl, bs, run));
       // G <- Q^T G Q  (X = G Q, G = X^T Q by symmetry),  Z <- Z Q
       if (!ident[r]) {                                   // G' in T, Z' in T2; Gp, Zp are free
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gr, n, 0, Q, m, Gp);     // Gp = (T) Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gr, n, 0, Q, m, Gp, run);     // Gp = (T) Q
         SCSF_LAUNCH_CHECK();
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 1, Q, m, T);      // T = Gp^T Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 1, Q, m, T, run);      // T = Gp^T Q
         SCSF_LAUNCH_CHECK();
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zr, n, 0, Q, m, Zp);     // Zp = T2 Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zr, n, 0, Q, m, Zp, run);     // Zp = T2 Q
         SCSF_LAUNCH_CHECK();
-        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T, Gp, (int64_t)n * n);
+        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T, Gp, (int64_t)n * n, run);
         SCSF_LAUNCH_CHECK();
       } else {
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 0, Q, m, T);      // T = Gp Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Gp, n, 0, Q, m, T, run);      // T = Gp Q
         SCSF_LAUNCH_CHECK();
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(T, n, 1, Q, m, Gp);      // Gp = T^T Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(T, n, 1, Q, m, Gp, run);      // Gp = T^T Q
         SCSF_LAUNCH_CHECK();
-        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zp, n, 0, Q, m, T2);     // T2 = Zp Q
+        k_bj_blkmm<<<dim3(ceil_div(n, BJ_R), P), 256, smm, bs>>>(Zp, n, 0, Q, m, T2, run);     // T2 = Zp Q
         SCSF_LAUNCH_CHECK();
-        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T2, Zp, (int64_t)n * n);
+        k_bj_copy<<<ceil_div((int64_t)n * n, 1024), 256, 0, bs>>>(T2, Zp, (int64_t)n * n, run);
         SCSF_LAUNCH_CHECK();
       }
     }
-    k_bj_offmax<<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, max_sweeps, ctrl, loop);
+    k_bj_offmax<<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, cap, ctrl, loop);
     SCSF_LAUNCH_CHECK();
     return SCSF_OK;
   };
-  SCSF_TRY(device_while(s, flag_d, t_flag, max_sweeps, sweep));
+  if (unroll > 0) {
+    DevLoop flag_only;
+    flag_only.flag = flag_d;
+    for (int k = 0; k < unroll; ++k) SCSF_TRY(sweep(s, flag_only));
+  } else {
+    SCSF_TRY(device_while(s, flag_d, t_flag, max_sweeps, sweep));
+  }
   k_bj_final<<<1, 512, 0, s>>>(Gp, Zp, n, A_last, w, b, theta, Zout);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;

@@ -355,8 +355,9 @@ __global__ void __launch_bounds__(JG_T, 1) k_jacobi_g(const double* __restrict__
                                                       double2* __restrict__ rec, int* __restrict__ recm,
                                                       int* __restrict__ nrec_out, double* __restrict__ theta_out,
                                                       int* __restrict__ rank_out, int max_sweeps, Ctrl* ctrl,
-                                                      int64_t gstride, int match_diag) {
+                                                      int64_t gstride, int match_diag, const int* skip) {
   constexpr int B = 1 << LOGB;
+  if (skip && *(volatile const int*)skip == 0) return;   // block Jacobi: this unrolled sweep is not needed
   // batch (block Jacobi): CTA z works on the z-th diagonal sub-matrix and its own record slots
   Gin += (int64_t)blockIdx.x * gstride;
   rec += (int64_t)blockIdx.x * JREC_SWEEPS * 128 * 64;
@@ -541,7 +542,8 @@ constexpr int JZ_T = 512;
 template <int LOGB>
 __global__ void __launch_bounds__(JZ_T) k_jacobi_z(const double2* __restrict__ rec, const int* __restrict__ recm,
                                                    const int* __restrict__ nrec_p, const int* __restrict__ rank,
-                                                   int b, double* __restrict__ Zout) {
+                                                   int b, double* __restrict__ Zout, const int* skip) {
+  if (skip && *(volatile const int*)skip == 0) return;
   rec += (int64_t)blockIdx.y * JREC_SWEEPS * 128 * 64;      // batch: sub-problem blockIdx.y
   recm += blockIdx.y * JREC_SWEEPS * 128;
   nrec_p += blockIdx.y;
@@ -982,16 +984,16 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
 template <int LOGB>
 static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scratch, double* theta, double* Zout,
                                Ctrl* ctrl, cudaStream_t s, int batch = 1, int64_t gstride = 0, int match = 0,
-                               int max_sweeps = 40) {
+                               int max_sweeps = 40, const int* skip = nullptr) {
   constexpr int B = 1 << LOGB;
   double2* rec = reinterpret_cast<double2*>(scratch);
   int* recm = reinterpret_cast<int*>(scratch + (size_t)batch * JREC_SWEEPS * 128 * 64 * 2);
   int* nrec = recm + batch * JREC_SWEEPS * 128;
   int* rank = nrec + 32;
   k_jacobi_g<LOGB><<<batch, JG_T, B * (B + 1) * sizeof(double), s>>>(G, ldg, b, rec, recm, nrec, theta, rank,
-                                                                     max_sweeps, ctrl, gstride, match);
+                                                                     max_sweeps, ctrl, gstride, match, skip);
   SCSF_LAUNCH_CHECK();
-  k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), JZ_T, 0, s>>>(rec, recm, nrec, rank, b, Zout);
+  k_jacobi_z<LOGB><<<dim3(ceil_div(b, 16), batch), JZ_T, 0, s>>>(rec, recm, nrec, rank, b, Zout, skip);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
@@ -1011,12 +1013,12 @@ static int bj_inner() {
   return v;
 }
 int jacobi_batched_impl(const double* G, int64_t ldg, int bs, int batch, int64_t gstride, double* scratch,
-                        double* theta, double* Q, Ctrl* ctrl, cudaStream_t s) {
+                        double* theta, double* Q, Ctrl* ctrl, cudaStream_t s, const int* skip) {
   const int inner = bj_inner();
   Ctrl* c = inner >= 40 ? ctrl : nullptr;
-  if (bs <= 32) return jacobi_split_launch<5>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner);
-  if (bs <= 64) return jacobi_split_launch<6>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner);
-  if (bs <= 128) return jacobi_split_launch<7>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner);
+  if (bs <= 32) return jacobi_split_launch<5>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner, skip);
+  if (bs <= 64) return jacobi_split_launch<6>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner, skip);
+  if (bs <= 128) return jacobi_split_launch<7>(G, ldg, bs, scratch, theta, Q, c, s, batch, gstride, 1, inner, skip);
   set_error("jacobi_batched: sub-problem %d > 128", bs);
   return SCSF_ERR_NOT_IMPLEMENTED;
 }

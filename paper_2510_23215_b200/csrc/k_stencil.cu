@@ -1079,9 +1079,9 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
     const double* __restrict__ cf, int64_t ldc, int nx, int64_t n_glob, int64_t goff, int64_t n_loc,
     const double* __restrict__ X, const double* Xp, double* Out, int64_t ldv, int ncols,
     const double* __restrict__ ghost_lo, const double* __restrict__ ghost_hi, const double* __restrict__ fp,
-    int step) {
-  const int64_t l0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;   // local point
-  if (l0 >= ldv) return;
+    int step, int64_t l_begin, int64_t l_end) {
+  const int64_t l0 = l_begin + ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;   // local point
+  if (l0 >= l_end) return;
   double a, b, c;
   step_scalars(fp, step, a, b, c);
   const int j0 = blockIdx.y * CB;
@@ -1132,18 +1132,36 @@ int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncol
   return SCSF_OK;
 }
 
+// part: 0 = every point of the slab (and the ld padding); 1 = the interior rows, which need no
+// ghost row (and the padding); 2 = the first and last row, which read the ghosts.  Parts 1 and 2
+// together equal part 0, so the halo exchange can run while part 1 computes.
 int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
                       double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
-                      const double* fp, int step, cudaStream_t s) {
+                      const double* fp, int step, cudaStream_t s, int part) {
   if (ncols <= 0) return SCSF_OK;
   const int64_t n_glob = (int64_t)ops->nx * ops->ny;
+  const int nx = ops->nx;
   const double* cf = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
   constexpr int CB = 4;                // 4 columns per CTA share the coefficient registers
-  dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
-  k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
-                                              ghost_lo, ghost_hi, fp, step);
-  SCSF_LAUNCH_CHECK();
-  return SCSF_OK;
+  auto launch = [&](int64_t lb, int64_t le) -> int {
+    if (le <= lb) return SCSF_OK;
+    dim3 g(ceil_div(ceil_div(le - lb, 4), SV_THREADS), ceil_div(ncols, CB));
+    k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
+                                                ghost_lo, ghost_hi, fp, step, lb, le);
+    SCSF_LAUNCH_CHECK();
+    return SCSF_OK;
+  };
+  const int64_t rows = n_loc / nx;
+  if (part == 0 || rows < 3) {
+    if (part == 2) return SCSF_OK;       // (rows < 3: part 1 already did everything)
+    return launch(0, ldv);
+  }
+  if (part == 1) {
+    SCSF_TRY(launch(nx, n_loc - nx));
+    return launch(n_loc, ldv);                          // padding
+  }
+  SCSF_TRY(launch(0, nx));
+  return launch(n_loc - nx, n_loc);
 }
 
 // ---------------------------------------------------------- residuals ----

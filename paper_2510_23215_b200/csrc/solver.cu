@@ -64,7 +64,7 @@ int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncol
                    double* send_hi, cudaStream_t s);
 int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
                       double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
-                      const double* fp, int step, cudaStream_t s);
+                      const double* fp, int step, cudaStream_t s, int part = 0);
 int colmax_local_impl(const double* V, int64_t ldv, int64_t n, const int* perm, int b, int64_t goff, double* colbuf,
                       cudaStream_t s);
 int sort_theta_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
@@ -205,13 +205,50 @@ static int gram(SolveWS& w, const double* X, int b1, const double* Y, int b2, in
 }
 
 // One stencil application (filter step `step`, or A X when step < 0) on ncols columns.
+// Row partition: the slab's boundary rows are packed and exchanged with the neighbours on a side
+// stream while the interior rows (which need no ghost row) compute on the solver's stream; the
+// first and last rows follow once the ghosts have landed (fork / join by events, capturable).
+struct HaloStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t packed = nullptr, landed = nullptr;
+};
+static int halo_streams(HaloStreams*& hs) {
+  static thread_local HaloStreams t;
+  if (!t.side) {
+    SCSF_CUDA_CHECK(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
+    SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&t.packed, cudaEventDisableTiming));
+    SCSF_CUDA_CHECK(cudaEventCreateWithFlags(&t.landed, cudaEventDisableTiming));
+  }
+  hs = &t;
+  return SCSF_OK;
+}
+static bool halo_overlap() {                       // SCSF_HALO_OVERLAP=0: exchange, then one stencil launch
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_HALO_OVERLAP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const double* Xp, double* Out, int ncols,
                 int step, cudaStream_t s, const int* deg = nullptr) {
   if (!w.comm) return stencil_impl(ops, op, X, Xp, Out, w.ldv, ncols, w.fp, step, s, deg);
+  const double* glo = w.comm->rank > 0 ? w.recv_lo : nullptr;
+  const double* ghi = w.comm->rank + 1 < w.comm->world ? w.recv_hi : nullptr;
   SCSF_TRY(pack_rows_impl(X, w.ldv, w.n, w.nx, ncols, w.send_lo, w.send_hi, s));
-  SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
-  return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, w.comm->rank > 0 ? w.recv_lo : nullptr,
-                           w.comm->rank + 1 < w.comm->world ? w.recv_hi : nullptr, w.fp, step, s);
+  if (!halo_overlap() || w.comm->world == 1) {
+    SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
+    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0);
+  }
+  HaloStreams* hs;
+  SCSF_TRY(halo_streams(hs));
+  SCSF_CUDA_CHECK(cudaEventRecord(hs->packed, s));
+  SCSF_CUDA_CHECK(cudaStreamWaitEvent(hs->side, hs->packed, 0));
+  SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, hs->side));
+  SCSF_CUDA_CHECK(cudaEventRecord(hs->landed, hs->side));
+  SCSF_TRY(stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 1));
+  SCSF_CUDA_CHECK(cudaStreamWaitEvent(s, hs->landed, 0));
+  return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 2);
 }
 
 // Q = CholQR pass on columns [0, ncols) of Y (in place, or into Out when Out != Y).
@@ -388,8 +425,8 @@ static int clear_chol_flag(SolveWS& w, cudaStream_t s) {
 struct GraphKey {
   // every device pointer an iteration's launches capture, and every shape / kernel choice:
   // a cached graph is replayed only on the exact buffers and operator kind it was captured for
-  const void *V, *W, *T1, *T2, *P, *ctrl, *fp, *coef;
-  int64_t n, ldv, ld, dims;
+  const void *V, *W, *T1, *T2, *P, *ctrl, *fp, *coef, *comm;
+  int64_t n, ldv, ld, dims, goff;
   int b, kL, degree, L, timing, stencil, ncoef, deg_on;
   double tol;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
@@ -487,7 +524,9 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
   // degrees (Alg. 1 l. 5's staggered update) chosen by k_lock, capped at |degree_arg|
   const bool adaptive = degree_arg < 0;
   const int degree = adaptive ? -degree_arg : degree_arg;
-  const bool graphs = graphs_enabled() && !w.comm && s != nullptr && !g_timing;
+  // (row partition: only a communicator whose collectives are stream-ordered device work (NCCL) can be
+  // captured; the loopback backend meets at host barriers)
+  const bool graphs = graphs_enabled() && (!w.comm || w.comm->capturable()) && s != nullptr && !g_timing;
   // With graphs, the operator's arrays are first copied into the chain's own
   // buffer, so every captured iteration is independent of the operator index.
   scsf_ops opl = *ops_in;
@@ -590,6 +629,8 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
       key.ctrl = w.ctrl;
       key.fp = w.fp;
       key.coef = ops->coef + (int64_t)op * ncoef(ops) * ops->ld;
+      key.comm = w.comm;
+      key.goff = w.goff;
       key.n = w.n;
       key.ldv = w.ldv;
       key.ld = ops->ld;

@@ -7,7 +7,7 @@ midpoints, following the recipe stated in DESIGN.md §3.
 Both sides consume the arrays it produces; neither side imports the other.
 """
 from .configs import CONFIGS, Config, get_config
-from .grf import OperatorFields, make_fields, make_batch, grf_std, constant_fields, draw_xi
+from .grf import OperatorFields, make_fields, make_batch, make_perturbed, grf_std, constant_fields, draw_xi
 
-__all__ = ["CONFIGS", "Config", "get_config", "OperatorFields", "make_fields",
+__all__ = ["CONFIGS", "Config", "get_config", "OperatorFields", "make_fields", "make_perturbed",
            "make_batch", "grf_std", "constant_fields", "draw_xi"]

@@ -217,3 +217,26 @@ def constant_fields(dim: int, nx: int, n_ops: int = 1, a: float = 1.0, c: float 
     cc = np.full((n_ops, n), float(c))
     params = np.full((n_ops, 1, n), float(a))
     return OperatorFields(dim, nx, 1.0 / (nx + 1), faces, cc, params)
+
+
+def make_perturbed(cfg: Config, n_ops: int, size: float, base: int = 0) -> OperatorFields:
+    """SURVEY f1, the paper's similarity experiment (tab:perturbation_impact): n_ops
+    perturbations of one base operator of a "lapv" config (-Lap u + V u, the paper's Helmholtz
+    stand-in).  V_i = V_base * exp(size * g_i / s_K), g_i an independent GRF of the config's recipe
+    scaled to unit domain-RMS, so `size` is the RMS relative perturbation (0.5, 0.1, 0.01, 0 in the
+    paper's table).  Deterministic: seeds (23215, 90, i, 0) for the perturbations."""
+    if cfg.family != "lapv":
+        raise ValueError("perturbation batches are defined for the -Lap u + V u family")
+    n = cfg.nx ** cfg.dim
+    g0, _ = make_fields(cfg, base, 0)
+    unit = cfg.with_(sigma=1.0)
+    faces = []
+    for ax in range(cfg.dim):
+        s = [cfg.nx] * cfg.dim
+        s[cfg.dim - 1 - ax] = cfg.nx + 1
+        faces.append(np.ones((n_ops,) + tuple(s)))
+    c = np.empty((n_ops, n))
+    for i in range(n_ops):
+        gi, _ = make_fields(unit, i, 0, cfg_index=90)
+        c[i] = (cfg.vscale * np.exp(g0 + size * gi)).reshape(n)
+    return OperatorFields(cfg.dim, cfg.nx, cfg.h, faces, c, c[:, None, :].copy())

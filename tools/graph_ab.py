@@ -25,7 +25,8 @@ else:
     ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).to(dev))
 perm, _, _ = scsf.sort(params, cfg.dim, cfg.nx, cfg.p0)
 ws = scsf._workspace(scsf.solve_workspace(ops, cfg.L, cfg.nex).numel() * C, dev)
-out = {"config": name, "N": N, "chains": C, "m": m, "graphs": os.environ.get("SCSF_GRAPHS", "1")}
+out = {"config": name, "N": N, "chains": C, "m": m, "graphs": os.environ.get("SCSF_GRAPHS", "1"),
+       "bj_unroll": os.environ.get("SCSF_BJ_UNROLL", "0")}
 for rep in range(3):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -37,4 +38,6 @@ for rep in range(3):
     its = sum(s["iterations"] for s in st)
     out[f"pass{rep}_ms"] = e0.elapsed_time(e1)
     out["iterations_total"] = its
+    out["jacobi_sweeps_per_iteration"] = sum(s["jacobi_sweeps"] for s in st) / max(its, 1)
+    out["converged"] = sum(s["status"] == 0 for s in st)
 print(json.dumps(out), flush=True)
