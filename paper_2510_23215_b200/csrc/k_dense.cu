@@ -14,7 +14,11 @@
 //            alias X (in-place rotation).
 #include "common.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <mutex>
 
 namespace scsf {
 
@@ -243,6 +247,201 @@ __global__ void __launch_bounds__(V2_NT) k_gemm_tn2(const double* __restrict__ X
         const int i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + 2 * t + e;
         if (i < b1 && j < b2) out[i + (int64_t)(j + jout) * b1] = acc[mi][ni][e];
       }
+}
+
+// =====================================================================
+// TN with TMA: the same 64 x 64 split-K Gram tile, operands delivered by the tensor-memory
+// accelerator.  One producer warp (one elected lane) streams 16-row x 64-column boxes of X and
+// Y (cp.async.bulk.tensor.2d, 128-byte swizzle, rows / columns past the operand zero-filled by
+// the hardware) into a TNT_ST-stage ring guarded by mbarriers (full: expect_tx bytes; empty:
+// one arrive per consumer warp); the 4 consumer warps run the DMMA loop.  No per-thread address
+// arithmetic or cp.async groups, and no CTA-wide barrier per chunk.
+//
+// Swizzled layout: a box lands as 64 rows of 128 B (one per X column), the 16-byte unit u of
+// row c stored at unit u ^ (c & 7).  A fragment row g of DMMA block mi reads X column
+// 4 g + mi (B: Y column 4 g + ni) of the warp's 32, so the 8 lanes of a 128-bit shared-load
+// phase (g = 2p, 2p+1) hit units t ^ mi and t ^ (4 + mi): 8 distinct units, conflict-free.
+// =====================================================================
+constexpr int TNT_ST = 6, TNT_BOX_R = 16, TNT_NT = 160;
+constexpr int TNT_TILE_BYTES = V2_T * TNT_BOX_R * 8;          // 8 KB per operand box
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(TNT_NT) k_gemm_tn_tma(const __grid_constant__ CUtensorMap tmX,
+                                                      const __grid_constant__ CUtensorMap tmY,
+                                                      const __grid_constant__ CUtensorMap tmY2, int dual, int b1,
+                                                      int b2, int64_t n, int64_t kchunk, int upper,
+                                                      double* __restrict__ P) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  // 1024-byte aligned ring: [TNT_ST] x {X box, Y box}; then the barriers
+  unsigned char* base = tsm + ((1024 - (smem_u32(tsm) & 1023)) & 1023);
+  const uint32_t ring = smem_u32(base);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TNT_ST * 2 * TNT_TILE_BYTES);
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * TNT_ST;
+
+  const int T2 = (b2 + V2_T - 1) / V2_T;
+  const int grp = dual ? (int)blockIdx.y / T2 : 0;
+  const int ti = blockIdx.x, tj = dual ? (int)blockIdx.y % T2 : (int)blockIdx.y;
+  if (upper && ti > tj) return;
+  const int i0 = ti * V2_T, j0 = tj * V2_T;
+  const int b2tot = dual ? 2 * b2 : b2;
+  const int jout = grp * b2;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = min(n, kbeg + kchunk);
+  const int nck = (int)((kend - kbeg + TNT_BOX_R - 1) / TNT_BOX_R);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int st = 0; st < TNT_ST; ++st) {
+      mbar_init(full0 + 8 * st, 1);
+      mbar_init(empty0 + 8 * st, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 4) {                                   // producer
+    if (lane == 0) {
+      const CUtensorMap* my = grp ? &tmY2 : &tmY;
+      for (int c = 0; c < nck; ++c) {
+        const int st = c % TNT_ST;
+        if (c >= TNT_ST) mbar_wait(empty0 + 8 * st, ((c / TNT_ST) - 1) & 1);
+        const uint32_t fb = full0 + 8 * st;
+        mbar_expect_tx(fb, 2 * TNT_TILE_BYTES);
+        const int k0 = (int)(kbeg + (int64_t)c * TNT_BOX_R);
+        tma_load_2d(ring + st * 2 * TNT_TILE_BYTES, &tmX, k0, i0, fb);
+        tma_load_2d(ring + st * 2 * TNT_TILE_BYTES + TNT_TILE_BYTES, my, k0, j0, fb);
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const bool idle = (i0 + wm >= b1) || (j0 + wn >= b2) || (upper && ti == tj && wm > wn);
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int c = 0; c < nck; ++c) {
+    const int st = c % TNT_ST;
+    mbar_wait(full0 + 8 * st, (c / TNT_ST) & 1);
+    if (!idle) {
+      const unsigned char* xs = base + st * 2 * TNT_TILE_BYTES;
+      const unsigned char* ys = xs + TNT_TILE_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < TNT_BOX_R; kk += 8) {
+        const int u = (kk >> 1) + t;               // 16-byte unit: rows kk + 2t, kk + 2t + 1
+        double2 a[4], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int col = wm + 4 * g + mi;
+          a[mi] = *reinterpret_cast<const double2*>(xs + col * 128 + ((u ^ (col & 7)) << 4));
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const int col = wn + 4 * g + ni;
+          b[ni] = *reinterpret_cast<const double2*>(ys + col * 128 + ((u ^ (col & 7)) << 4));
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);     // this warp is done with the stage
+  }
+  double* out = P + (int64_t)blockIdx.z * b1 * b2tot;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wm + 4 * g + mi, j = j0 + wn + 4 * (2 * t + e) + ni;
+        if (i < b1 && j < b2) out[i + (int64_t)(j + jout) * b1] = acc[mi][ni][e];
+      }
+}
+static size_t tnt_smem() { return (size_t)TNT_ST * 2 * TNT_TILE_BYTES + 2 * 8 * TNT_ST + 1024; }
+
+// Tensor map of a column-major n x cols operand (ld doubles): dim 0 = rows (contiguous), dim 1 =
+// columns, box 16 rows x 64 columns, 128-byte swizzle; out-of-range rows / columns read as zero.
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int tma_encode_fn() {
+  static std::once_flag once;
+  static int status = SCSF_OK;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      status = SCSF_ERR_DEVICE;
+      return;
+    }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (status != SCSF_OK) set_error("cuTensorMapEncodeTiled is not available from the driver");
+  return status;
+}
+static int make_tmap(CUtensorMap* m, const double* X, int64_t ld, int64_t n, int cols) {
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {TNT_BOX_R, V2_T};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): n %lld, cols %d, ld %lld", (int)r, (long long)n, cols, (long long)ld);
+    return SCSF_ERR_DEVICE;
+  }
+  return SCSF_OK;
+}
+// SCSF_TN_TMA=0 keeps the cp.async kernel (k_gemm_tn2) for A/B runs
+static bool tn_tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_TN_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// TMA needs 16-byte aligned bases and leading dimensions (ld even) and row counts >= 16 to pay
+static bool tma_ok(const double* p, int64_t ld, int64_t n) {
+  return tn_tma_enabled() && ((uintptr_t)p & 15) == 0 && (ld & 1) == 0 && n >= 64 && n < (1ll << 31);
 }
 
 // ---- NN: Out[r0:r0+64, :] = alpha X[r0:r0+64, 0:b1] M + beta Out.  The whole
@@ -543,6 +742,7 @@ int dense_init_attrs() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        NN_MAX_K * NN_LDS * (int)sizeof(double)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn2_smem()));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tnt_smem()));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn2_smem(NN2_MAX_K)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -598,8 +798,15 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   int64_t kchunk = round_up(ceil_div(n, splits), TN_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
-  const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
-  k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
+  if (tma_ok(X, ldx, n) && tma_ok(Y, ldy, n) && tma_encode_fn() == SCSF_OK) {
+    CUtensorMap mx, my;
+    SCSF_TRY(make_tmap(&mx, X, ldx, n, b1));
+    SCSF_TRY(make_tmap(&my, Y, ldy, n, b2));
+    k_gemm_tn_tma<<<g, TNT_NT, tnt_smem(), s>>>(mx, my, my, 0, b1, b2, n, kchunk, upper, P);
+  } else {
+    const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
+    k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
+  }
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b1, 32), b2);
   k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b1, b2, alpha, upper, b2, C, ldc);
@@ -620,9 +827,17 @@ int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y
   int64_t kchunk = round_up(ceil_div(n, splits), TN_KC);
   splits = ceil_div(n, kchunk);
   dim3 g(t, 2 * t, splits);
-  const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
-                   ((uintptr_t)Y2 & 15) == 0) ? 1 : 0;
-  k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b, Y1, ldy, b, n, kchunk, 1, a16, P, Y2);
+  if (tma_ok(X, ldx, n) && tma_ok(Y1, ldy, n) && tma_ok(Y2, ldy, n) && tma_encode_fn() == SCSF_OK) {
+    CUtensorMap mx, m1, m2;
+    SCSF_TRY(make_tmap(&mx, X, ldx, n, b));
+    SCSF_TRY(make_tmap(&m1, Y1, ldy, n, b));
+    SCSF_TRY(make_tmap(&m2, Y2, ldy, n, b));
+    k_gemm_tn_tma<<<g, TNT_NT, tnt_smem(), s>>>(mx, m1, m2, 1, b, b, n, kchunk, 1, P);
+  } else {
+    const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
+                     ((uintptr_t)Y2 & 15) == 0) ? 1 : 0;
+    k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b, Y1, ldy, b, n, kchunk, 1, a16, P, Y2);
+  }
   SCSF_LAUNCH_CHECK();
   dim3 gr(ceil_div(b, 32), 2 * b);
   k_reduce_partials<<<gr, 256, 0, s>>>(P, splits, b, 2 * b, 1.0, 1, b, C, ldc);

@@ -326,7 +326,7 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   // residuals of A V by one stencil pass (cheaper than the n x b x b product W1 M); without a row
   // partition the pass is fused with the norms and W is not written (only the residuals use it)
   bool fused = false;
-  if (!w.comm && fused_resid())
+  if ((!w.comm || w.comm->world == 1) && fused_resid())   // (one slab: the whole operator, goff = 0)
     SCSF_TRY(stencil_resid_impl(ops, op, Va, w.ldv, ba, w.theta + k0, w.res + k0, w.wn + k0, w.P, s, &fused));
   if (!fused) {
     SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));

@@ -43,6 +43,19 @@ def test_gemm_tn(lib, n, b1, b2):
     assert np.all(np.abs(C - ref) <= 1e-13 * bound + 1e-300)
 
 
+@pytest.mark.parametrize("n,b1,b2,ld", [(1000, 65, 64, 1001), (4103, 200, 130, 4160), (40000, 240, 240, 40000),
+                                        (63, 3, 70, 64), (250000, 100, 37, 250016)])
+def test_gemm_tn_leading_dimensions(lib, n, b1, b2, ld):
+    """Odd ld (the cp.async kernel) and even ld (the TMA-fed kernel: 16-row boxes, rows past n and
+    columns past b zero-filled by the tensor map), ragged n and b, both against numpy."""
+    rng = np.random.default_rng(ld)
+    X = rng.standard_normal((n, b1))
+    Y = rng.standard_normal((n, b2))
+    C = lib.gemm_tn(_blk(X, ld), _blk(Y, ld), n).cpu().numpy().T
+    bound = np.abs(X).T @ np.abs(Y)
+    assert np.all(np.abs(C - X.T @ Y) <= 1e-13 * bound + 1e-300)
+
+
 @pytest.mark.parametrize("n,b", [(10000, 120), (3000, 70), (500, 240)])
 def test_gemm_tn_upper(lib, n, b):
     rng = np.random.default_rng(b)
