@@ -471,6 +471,147 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
   }
 }
 
+// ---- streaming step with grouped loads (k_stencil_v4g).  Same arithmetic as k_stencil_v4 (bitwise:
+// the same expressions in the same order), but for each group of G columns every global load of
+// the group is issued before any arithmetic, and the stores carry no compiler memory barrier, so
+// a thread keeps G columns of loads (up to 6 x 32 B each) in flight instead of one column's.
+__device__ __forceinline__ double4 ldg4_rd(const double* p) {     // Y_{s-1}: read once, before its own store
+  double4 v;
+  asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg4_nb(double* p, double4 v) {    // no "memory" clobber
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w));
+}
+
+template <int DIM, int CB, int G>
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4g(
+    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n,
+    const double* __restrict__ X, const double* Xp, double* Out,   // Out may alias Xp (same-index RMW)
+    int64_t ldv, int ncols, const double* __restrict__ fp, int step, const int* __restrict__ deg) {
+  const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
+  if (k0 >= ldv) return;
+  double a, b, c;
+  step_scalars(fp, step, a, b, c);
+  const int64_t sxy = (int64_t)nx * ny;
+  int j0 = blockIdx.y * CB;
+  const int j1 = min(ncols, j0 + CB);
+  if (deg)
+    while (j0 < j1 && __ldg(deg + j0) <= step) ++j0;
+  if (j0 >= j1) return;
+  if (k0 + 4 > n) {                                  // tail quad / padding: the plain kernel's path
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = k0 + q;
+      if (k >= ldv) break;
+      if (k >= n) {
+        for (int j = j0; j < j1; ++j) Out[(int64_t)j * ldv + k] = 0.0;
+        continue;
+      }
+      const double dg = cf[k] - c;
+      const double xp = cf[ldc + k], xm = (k >= 1) ? cf[ldc + k - 1] : 0.0;
+      const double yp = cf[2 * ldc + k], ym = (k >= nx) ? cf[2 * ldc + k - nx] : 0.0;
+      double zp = 0.0, zm = 0.0;
+      if (DIM == 3) {
+        zp = cf[3 * ldc + k];
+        zm = (k >= sxy) ? cf[3 * ldc + k - sxy] : 0.0;
+      }
+      for (int j = j0; j < j1; ++j) {
+        const double* x = X + (int64_t)j * ldv;
+        double v = dg * x[k];
+        if (k + 1 < n) v = fma(xp, x[k + 1], v);
+        if (k >= 1) v = fma(xm, x[k - 1], v);
+        if (k + nx < n) v = fma(yp, x[k + nx], v);
+        if (k >= nx) v = fma(ym, x[k - nx], v);
+        if (DIM == 3) {
+          if (k + sxy < n) v = fma(zp, x[k + sxy], v);
+          if (k >= sxy) v = fma(zm, x[k - sxy], v);
+        }
+        v *= a;
+        if (b != 0.0) v = fma(b, Xp[(int64_t)j * ldv + k], v);
+        Out[(int64_t)j * ldv + k] = v;
+      }
+    }
+    return;
+  }
+  const double4 z4 = make_double4(0, 0, 0, 0);
+  const double4 dg = ldg4_nc(cf + k0);
+  const double4 cxp = ldg4_nc(cf + ldc + k0);
+  const double cxm = (k0 >= 1) ? cf[ldc + k0 - 1] : 0.0;
+  const double4 cyp = ldg4_nc(cf + 2 * ldc + k0);
+  const bool hym = k0 >= nx, hyp = k0 + nx + 3 < n;
+  const double4 cym = hym ? ldg4_nc(cf + 2 * ldc + k0 - nx) : z4;
+  double4 czp = z4, czm = z4;
+  bool hzm = false, hzp = false;
+  if (DIM == 3) {
+    czp = ldg4_nc(cf + 3 * ldc + k0);
+    hzm = k0 >= sxy;
+    hzp = k0 + sxy + 3 < n;
+    if (hzm) czm = ldg4_nc(cf + 3 * ldc + k0 - sxy);
+  }
+  const bool hm = k0 >= 1, hp = k0 + 4 < n;
+  const bool usep = b != 0.0;
+#pragma unroll
+  for (int g0 = 0; g0 < CB; g0 += G) {
+    double4 xc[G], xu[G], xd[G], zu[G], zd[G], pp[G];
+    double xl[G], xr[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {                    // every load of the group first
+      const int j = j0 + g0 + q;
+      if (j < j1) {
+        const double* __restrict__ x = X + (int64_t)j * ldv;
+        xc[q] = ldg4_nc(x + k0);
+        xl[q] = hm ? __ldg(x + k0 - 1) : 0.0;
+        xr[q] = hp ? __ldg(x + k0 + 4) : 0.0;
+        xu[q] = hyp ? ldg4_nc(x + k0 + nx) : z4;
+        xd[q] = hym ? ldg4_nc(x + k0 - nx) : z4;
+        if (DIM == 3) {
+          zu[q] = hzp ? ldg4_nc(x + k0 + sxy) : z4;
+          zd[q] = hzm ? ldg4_nc(x + k0 - sxy) : z4;
+        }
+        pp[q] = usep ? ldg4_rd(Xp + (int64_t)j * ldv + k0) : z4;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int j = j0 + g0 + q;
+      if (j < j1) {
+        double4 v;
+        v.x = (dg.x - c) * xc[q].x + cxp.x * xc[q].y + cxm * xl[q] + cyp.x * xu[q].x + cym.x * xd[q].x;
+        v.y = (dg.y - c) * xc[q].y + cxp.y * xc[q].z + cxp.x * xc[q].x + cyp.y * xu[q].y + cym.y * xd[q].y;
+        v.z = (dg.z - c) * xc[q].z + cxp.z * xc[q].w + cxp.y * xc[q].y + cyp.z * xu[q].z + cym.z * xd[q].z;
+        v.w = (dg.w - c) * xc[q].w + cxp.w * xr[q] + cxp.z * xc[q].z + cyp.w * xu[q].w + cym.w * xd[q].w;
+        if (DIM == 3) {
+          v.x += czp.x * zu[q].x + czm.x * zd[q].x;
+          v.y += czp.y * zu[q].y + czm.y * zd[q].y;
+          v.z += czp.z * zu[q].z + czm.z * zd[q].z;
+          v.w += czp.w * zu[q].w + czm.w * zd[q].w;
+        }
+        v.x *= a; v.y *= a; v.z *= a; v.w *= a;
+        if (usep) {
+          v.x = fma(b, pp[q].x, v.x); v.y = fma(b, pp[q].y, v.y); v.z = fma(b, pp[q].z, v.z); v.w = fma(b, pp[q].w, v.w);
+        }
+        stg4_nb(Out + (int64_t)j * ldv + k0, v);
+      }
+    }
+  }
+}
+
+// Columns whose loads are issued together.  Measured (tools/bench_filter.py, streaming filter at
+// m = 20, fraction of the measured HBM copy rate, plain k_stencil_v4 / G = 1 / 2 / 4):
+// C3 0.71 / 0.80 / 0.85 / 0.64, C4 (3-D) 0.51 / 0.66 / 0.53 / 0.48, C5 0.84 / 0.94 / 0.98 / 0.70
+// (profiles/r02_stencil_groups.json); default G = 2 in 2-D (124 registers), G = 1 in 3-D (126;
+// G = 2 needs 204 and halves the resident warps).  SCSF_V4_GROUP = 0 (plain), 1, 2, 4 overrides.
+static int v4_group(int dim) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SCSF_V4_GROUP");
+    v = e ? atoi(e) : -1;
+    if (v != 0 && v != 1 && v != 2 && v != 4) v = -1;
+  }
+  return v >= 0 ? v : (dim == 2 ? 2 : 1);
+}
+
 // ------------------------------------------- column-resident filter (2-D) ----
 // All m steps of Alg. 1 for one column in one CTA (small grids, n <= RES_MAX_N):
 // Y_s double-buffered in shared memory, Y_{s-1} of the thread's own points in
@@ -1099,28 +1240,45 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
   const double4 cym = hym ? ldg4_nc(cf + 2 * ldc + k0 - nx) : make_double4(0, 0, 0, 0);
   const bool hm = l0 >= 1, hp = l0 + 4 < n_loc;       // x-neighbours never leave the slab row
   const bool dn_in = l0 >= nx, up_in = l0 + nx < n_loc;
+  const bool usep = b != 0.0;
+  const double4 z4 = make_double4(0, 0, 0, 0);
+  // two columns at a time, every load of the pair issued before any arithmetic (as k_stencil_v4g)
+  constexpr int G = 2;
 #pragma unroll
-  for (int jj = 0; jj < CB; ++jj) {
-    const int j = j0 + jj;
-    if (j >= j1) break;
-    const double* __restrict__ x = X + (int64_t)j * ldv;
-    const double4 xc = ldg4_nc(x + l0);
-    const double xl = hm ? x[l0 - 1] : 0.0;
-    const double xr = hp ? x[l0 + 4] : 0.0;
-    double4 xu = make_double4(0, 0, 0, 0), xd = make_double4(0, 0, 0, 0);
-    if (hyp) xu = up_in ? ldg4_nc(x + l0 + nx) : ldg4_nc(ghost_hi + (int64_t)j * nx + (l0 + nx - n_loc));
-    if (hym) xd = dn_in ? ldg4_nc(x + l0 - nx) : ldg4_nc(ghost_lo + (int64_t)j * nx + l0);
-    double4 v;
-    v.x = (dg.x - c) * xc.x + cxp.x * xc.y + cxm * xl + cyp.x * xu.x + cym.x * xd.x;
-    v.y = (dg.y - c) * xc.y + cxp.y * xc.z + cxp.x * xc.x + cyp.y * xu.y + cym.y * xd.y;
-    v.z = (dg.z - c) * xc.z + cxp.z * xc.w + cxp.y * xc.y + cyp.z * xu.z + cym.z * xd.z;
-    v.w = (dg.w - c) * xc.w + cxp.w * xr + cxp.z * xc.z + cyp.w * xu.w + cym.w * xd.w;
-    v.x *= a; v.y *= a; v.z *= a; v.w *= a;
-    if (b != 0.0) {
-      const double4 p = ldg4(Xp + (int64_t)j * ldv + l0);
-      v.x = fma(b, p.x, v.x); v.y = fma(b, p.y, v.y); v.z = fma(b, p.z, v.z); v.w = fma(b, p.w, v.w);
+  for (int g0 = 0; g0 < CB; g0 += G) {
+    double4 xc[G], xu[G], xd[G], pp[G];
+    double xl[G], xr[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int j = j0 + g0 + q;
+      if (j < j1) {
+        const double* __restrict__ x = X + (int64_t)j * ldv;
+        xc[q] = ldg4_nc(x + l0);
+        xl[q] = hm ? __ldg(x + l0 - 1) : 0.0;
+        xr[q] = hp ? __ldg(x + l0 + 4) : 0.0;
+        xu[q] = z4;
+        xd[q] = z4;
+        if (hyp) xu[q] = up_in ? ldg4_nc(x + l0 + nx) : ldg4_nc(ghost_hi + (int64_t)j * nx + (l0 + nx - n_loc));
+        if (hym) xd[q] = dn_in ? ldg4_nc(x + l0 - nx) : ldg4_nc(ghost_lo + (int64_t)j * nx + l0);
+        pp[q] = usep ? ldg4_rd(Xp + (int64_t)j * ldv + l0) : z4;
+      }
     }
-    stg4(Out + (int64_t)j * ldv + l0, v);
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int j = j0 + g0 + q;
+      if (j < j1) {
+        double4 v;
+        v.x = (dg.x - c) * xc[q].x + cxp.x * xc[q].y + cxm * xl[q] + cyp.x * xu[q].x + cym.x * xd[q].x;
+        v.y = (dg.y - c) * xc[q].y + cxp.y * xc[q].z + cxp.x * xc[q].x + cyp.y * xu[q].y + cym.y * xd[q].y;
+        v.z = (dg.z - c) * xc[q].z + cxp.z * xc[q].w + cxp.y * xc[q].y + cyp.z * xu[q].z + cym.z * xd[q].z;
+        v.w = (dg.w - c) * xc[q].w + cxp.w * xr[q] + cxp.z * xc[q].z + cyp.w * xu[q].w + cym.w * xd[q].w;
+        v.x *= a; v.y *= a; v.z *= a; v.w *= a;
+        if (usep) {
+          v.x = fma(b, pp[q].x, v.x); v.y = fma(b, pp[q].y, v.y); v.z = fma(b, pp[q].z, v.z); v.w = fma(b, pp[q].w, v.w);
+        }
+        stg4_nb(Out + (int64_t)j * ldv + l0, v);
+      }
+    }
   }
 }
 
@@ -1482,12 +1640,23 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
     // the HBM peak with CB = 2 / 4: C3 0.74 / 0.75, C4 (3-D) 0.60 / 0.68, C5 0.85 / 0.88)
     constexpr int CB = 4;
     dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
-    if (ops->dim == 2)
+    const int grp = v4_group(ops->dim);
+#define SCSF_V4G(D, G)                                                                                          \
+  k_stencil_v4g<D, CB, G><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, \
+                                                   step, deg)
+    if (grp == 1) {
+      if (ops->dim == 2) SCSF_V4G(2, 1); else SCSF_V4G(3, 1);
+    } else if (grp == 2) {
+      if (ops->dim == 2) SCSF_V4G(2, 2); else SCSF_V4G(3, 2);
+    } else if (grp == 4) {
+      if (ops->dim == 2) SCSF_V4G(2, 4); else SCSF_V4G(3, 4);
+    } else if (ops->dim == 2)
       k_stencil_v4<2, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step,
                                                    deg);
     else
       k_stencil_v4<3, CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, step,
                                                    deg);
+#undef SCSF_V4G
   } else {
     if (deg) {
       set_error("per-column filter degrees need the vectorised stencil (nx %% 4 == 0, aligned blocks)");

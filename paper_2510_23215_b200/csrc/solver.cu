@@ -235,8 +235,10 @@ static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const 
   if (!w.comm) return stencil_impl(ops, op, X, Xp, Out, w.ldv, ncols, w.fp, step, s, deg);
   const double* glo = w.comm->rank > 0 ? w.recv_lo : nullptr;
   const double* ghi = w.comm->rank + 1 < w.comm->world ? w.recv_hi : nullptr;
+  if (w.comm->world == 1)                          // one slab: no neighbour, no exchange
+    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0);
   SCSF_TRY(pack_rows_impl(X, w.ldv, w.n, w.nx, ncols, w.send_lo, w.send_hi, s));
-  if (!halo_overlap() || w.comm->world == 1) {
+  if (!halo_overlap()) {
     SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
     return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0);
   }
