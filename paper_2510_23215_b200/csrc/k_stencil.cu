@@ -751,8 +751,13 @@ __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
-template <int CS, int CB>
-__global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
+// REG: the thread keeps its own patch rows of Y_s and Y_{s-1} in registers (they are exactly what
+// it computed and stored in the two previous steps), so per step and column it reads only the
+// rows below / above its patch and the warp-edge x-neighbours from shared memory: 2 (+ edge)
+// loads instead of 6 (ncu on C3: the kernel waits on the shared-memory instruction queue).
+constexpr int CL_T_REG = 704;                    // REG variant: <= 93 registers (C3: 7 x 100 patches)
+template <int CS, int CB, bool REG = false>
+__global__ void __launch_bounds__(REG ? CL_T_REG : CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
                                                        const int* __restrict__ deg) {
@@ -858,6 +863,15 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
   const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
+  double2 ysa[CB], ysb[CB], ypa[CB], ypb[CB];              // REG: own rows of Y_s, Y_{s-1}
+  if (REG) {
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+      ysa[cc] = lds2a(acur[cc]);
+      ysb[cc] = lds2a(acur[cc] + nx8);
+      ypa[cc] = ypb[cc] = z2;                              // Y_{-1} = 0 (bco = 0 at s = 0)
+    }
+  }
   for (int st = 0; st < mrun; ++st) {
     const double a = sa[st], bco = sb[st];
 #pragma unroll
@@ -865,8 +879,9 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
       if (st < mcol[cc]) {                                 // uniform across the CTA (0 beyond ncb)
         const unsigned ca = acur[cc], na = anxt[cc];
         const double2 xd = lds2a(ca - nx8);
-        const double2 xa = lds2a(ca);
-        const double2 xb = lds2a(ca + nx8);
+        const double2 xa = REG ? ysa[cc] : lds2a(ca);
+        // (a patch without an upper row reads the ghost row above from shared memory, every step)
+        const double2 xb = (REG && up_ok) ? ysb[cc] : lds2a(ca + nx8);
         const double2 xu = lds2a(ca + up8);
         double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
         double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
@@ -884,9 +899,15 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
         u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
         // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
-        const double2 p0 = lds2a(na), p1 = lds2a(na + nx8);
+        const double2 p0 = REG ? ypa[cc] : lds2a(na), p1 = REG ? ypb[cc] : lds2a(na + nx8);
         v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
         u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
+        if (REG) {
+          ypa[cc] = xa;
+          ypb[cc] = xb;
+          ysa[cc] = v;
+          ysb[cc] = u;
+        }
         if (act) sts2a(na, v);
         if (up_ok) sts2a(na + nx8, u);
         // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas)
@@ -1405,7 +1426,7 @@ static int g_res_attr = 0;
 // (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
 // clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
 int stencil_init_attrs();
-template <int CS, int CB>
+template <int CS, int CB, bool REG>
 __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
                             const int* __restrict__ deg);
@@ -1498,6 +1519,10 @@ static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* c
                                 const int* deg) {
   if (cb == 4) return launch_cl1<CS, 4>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   if (cb == 2) return launch_cl1<CS, 2>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  if (cb == -2)                                            // register-resident patch rows, 2 columns
+    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, 2, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  if (cb == -1)
+    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, 1, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   return launch_cl1<CS, 1>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 static cudaError_t launch_rp(cudaLaunchConfig_t& cfg, int cs, const double* cf, int64_t ldc, int nx, int ny,
@@ -1538,6 +1563,13 @@ static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#define SCSF_CLR_ATTR(CS, CB) \
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+  SCSF_CLR_ATTR(1, 1); SCSF_CLR_ATTR(1, 2); SCSF_CLR_ATTR(2, 1); SCSF_CLR_ATTR(2, 2); SCSF_CLR_ATTR(4, 1);
+  SCSF_CLR_ATTR(4, 2); SCSF_CLR_ATTR(8, 1); SCSF_CLR_ATTR(8, 2); SCSF_CLR_ATTR(16, 1); SCSF_CLR_ATTR(16, 2);
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#undef SCSF_CLR_ATTR
 #undef SCSF_CL_ATTR
 #define SCSF_RP_ATTR(CS) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_rp<CS, RP_CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
@@ -1554,6 +1586,13 @@ int stencil_init_attrs() {
   return status;
 }
 
+
+// SCSF_FILTER_REG = 1 / 2: the register-resident-rows variant of k_filter_cl with 2 / 1 columns per
+// CTA (A/B switch; default off)
+static int filter_reg_cols() {                            // read per call (tests toggle it)
+  const char* e = getenv("SCSF_FILTER_REG");
+  return (e && e[0] == '1') ? 2 : (e && e[0] == '2') ? 1 : 0;
+}
 
 // Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
@@ -1586,12 +1625,14 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
   } else if (cs > 0) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
-    const int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
+    int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
     const int thr = (int)round_up((int64_t)(R / 2) * (ops->nx / 2), 32);
+    const int regc = thr <= CL_T_REG ? filter_reg_cols() : 0;
+    if (regc > 0) cb = -min(cb, regc);                     // register-resident rows: 1 or 2 columns per CTA
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs, ceil_div(ncols, cb), 1);
+    cfg.gridDim = dim3(cs, ceil_div(ncols, cb < 0 ? -cb : cb), 1);
     cfg.blockDim = dim3(thr, 1, 1);
-    cfg.dynamicSmemBytes = per_col * cb;
+    cfg.dynamicSmemBytes = per_col * (cb < 0 ? -cb : cb);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -1,6 +1,6 @@
 """One warm-start chain of a config (default C2, 6 operators) for ncu launch lists / captures.
 
-  python tools/profile_chain.py [CFG] [N_OPS] [CHAINS]
+  python tools/profile_chain.py [CFG] [N_OPS] [CHAINS] [DEGREE]
 """
 import sys
 import time
@@ -18,6 +18,7 @@ def main():
     nops = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     chains = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     cfg = synth.get_config(name)
+    m = int(sys.argv[4]) if len(sys.argv) > 4 else cfg.degree
     f = synth.make_batch(cfg, nops)
     dev = torch.device("cuda", 0)
     params = torch.from_numpy(f.params).to(dev)
@@ -30,10 +31,10 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if chains == 1:
-        ev, _, st = scsf.solve_queue(ops, perm, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter, seed=1,
+        ev, _, st = scsf.solve_queue(ops, perm, cfg.L, cfg.nex, m, cfg.tol, cfg.max_iter, seed=1,
                                      want_vecs=False, raise_on_fail=False)
     else:
-        ev, _, st = scsf.solve_chains(ops, perm, chains, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter,
+        ev, _, st = scsf.solve_chains(ops, perm, chains, cfg.L, cfg.nex, m, cfg.tol, cfg.max_iter,
                                       seed=1, want_vecs=False, raise_on_fail=False)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
