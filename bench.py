@@ -43,10 +43,10 @@ CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 # (tab:degree: "as long as m is chosen within a reasonable range, its specific value
 # does not significantly influence the performance"; fixed at 20 for its n <= 1e4 problems).
 # On the BASELINE configs the spectra are far wider (beta / lambda_L ~ 700 on C3), the degree-20
-# filter sits in its slow regime and the outer iterations are 4-7x those of m = 60-80 (DESIGN.md
-# reading R27, tools/degree_sweep.py, profiles/r02_degree_sweep.jsonl).  Every operator still
+# filter sits in its slow regime and the outer iterations are 4-10x those of m = 60-120 (DESIGN.md
+# reading R27, tools/degree_sweep.py, profiles/r02_degree_sweep*.jsonl).  Every operator still
 # converges to the same tolerance; the line also reports the paper's m = 20 on the same queue.
-BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 80, "C4": 80, "C5": 60}
+BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 120, "C4": 80, "C5": 80}
 DEFAULT_CONFIG = "C3"
 
 
@@ -264,10 +264,14 @@ def roofline_objects(scsf, cfg, ops, rst, r_ms, degree, step_ms_per_op, hbm, hbm
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            ent = tj.get(cfg.name) if isinstance(tj, dict) and cfg.name in tj else tj
+            ent = tj.get(cfg.name, {})
             if ent.get("config") == cfg.name and ent.get("filter_kind") == kind:
-                # ncu DRAM bytes of the profiled launch, scaled by this run's mean launch size
-                traffic = ent["dram_bytes_per_launch"] * (fbytes / max(launches_f, 1)) / ent["algorithmic_bytes_per_launch"]
+                # ncu DRAM bytes of the profiled whole-filter launch (Y_0 in, Y_m out: independent of the
+                # degree), scaled by this run's mean active columns per launch
+                m_ = abs(degree)
+                per = fbytes / max(launches_f, 1) - 8.0 * (1 + cfg.dim) * cfg.n * m_
+                cols = per / ((16.0 + 24.0 * (m_ - 1)) * cfg.n)
+                traffic = ent["dram_bytes_per_launch"] * cols / ent["columns"]
         except Exception:
             traffic = None
     hbm_obj = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",

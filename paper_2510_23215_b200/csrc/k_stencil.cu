@@ -724,6 +724,12 @@ constexpr int CL_MAXP = CL_T;                    // 2 x 2 patches per CTA
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
+}
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
@@ -751,13 +757,11 @@ __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
-// REG: the thread keeps its own patch rows of Y_s and Y_{s-1} in registers (they are exactly what
-// it computed and stored in the two previous steps), so per step and column it reads only the
-// rows below / above its patch and the warp-edge x-neighbours from shared memory: 2 (+ edge)
-// loads instead of 6 (ncu on C3: the kernel waits on the shared-memory instruction queue).
-constexpr int CL_T_REG = 704;                    // REG variant: <= 93 registers (C3: 7 x 100 patches)
-template <int CS, int CB, bool REG = false>
-__global__ void __launch_bounds__(REG ? CL_T_REG : CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
+// SPLIT: the per-step cluster barrier is split into arrive / wait, and the patches that read no
+// ghost row (not in the slab's first or last row: they need only their own CTA's previous step)
+// run between the two, hiding the cluster-wide synchronisation behind most of the step's work.
+template <int CS, int CB, bool SPLIT = false>
+__global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
                                                        const int* __restrict__ deg) {
@@ -863,62 +867,69 @@ __global__ void __launch_bounds__(REG ? CL_T_REG : CL_T, 1) k_filter_cl(const do
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
   const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
-  double2 ysa[CB], ysb[CB], ypa[CB], ypb[CB];              // REG: own rows of Y_s, Y_{s-1}
-  if (REG) {
-#pragma unroll
-    for (int cc = 0; cc < CB; ++cc) {
-      ysa[cc] = lds2a(acur[cc]);
-      ysb[cc] = lds2a(acur[cc] + nx8);
-      ypa[cc] = ypb[cc] = z2;                              // Y_{-1} = 0 (bco = 0 at s = 0)
-    }
-  }
+  const bool bnd = (lr0 == 0) || (lr0 + 2 >= rows);        // reads a ghost row (SPLIT)
   for (int st = 0; st < mrun; ++st) {
     const double a = sa[st], bco = sb[st];
+    if (SPLIT && st > 0) {
+      __syncwarp();
+      cluster_arrive();                                    // my stores of step st - 1 (incl. DSMEM pushes)
+      __syncthreads();                                     // this CTA's stores of step st - 1 are visible
+    }
 #pragma unroll
-    for (int cc = 0; cc < CB; ++cc) {
-      if (st < mcol[cc]) {                                 // uniform across the CTA (0 beyond ncb)
-        const unsigned ca = acur[cc], na = anxt[cc];
-        const double2 xd = lds2a(ca - nx8);
-        const double2 xa = REG ? ysa[cc] : lds2a(ca);
-        // (a patch without an upper row reads the ghost row above from shared memory, every step)
-        const double2 xb = (REG && up_ok) ? ysb[cc] : lds2a(ca + nx8);
-        const double2 xu = lds2a(ca + up8);
-        double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
-        double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
-        if (fix_l) {
-          xal = lds1a(ca - 8u);
-          xbl = lds1a(ca + nx8 - 8u);
+    for (int ph = 0; ph < (SPLIT ? 2 : 1); ++ph) {
+      if (SPLIT && ph == 1 && st > 0) {
+        __syncwarp();
+        cluster_wait();                                    // neighbours' ghost rows of step st - 1
+      }
+      if (SPLIT && ((ph == 0) == bnd)) continue;           // phase 0: interior patches, 1: boundary
+#pragma unroll
+      for (int cc = 0; cc < CB; ++cc) {
+        if (st < mcol[cc]) {                               // uniform across the CTA (0 beyond ncb)
+          const unsigned ca = acur[cc], na = anxt[cc];
+          const double2 xd = lds2a(ca - nx8);
+          const double2 xa = lds2a(ca);
+          const double2 xb = lds2a(ca + nx8);
+          const double2 xu = lds2a(ca + up8);
+          double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
+          double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
+          if (fix_l) {
+            xal = lds1a(ca - 8u);
+            xbl = lds1a(ca + nx8 - 8u);
+          }
+          if (fix_r) {
+            xar = lds1a(ca + 16u);
+            xbr = lds1a(ca + nx8 + 16u);
+          }
+          double2 v, u;
+          v.x = fma(dg0.x, xa.x, fma(cxp0.x, xa.y, fma(cxm0, xal, fma(cyp0.x, xb.x, cym0.x * xd.x))));
+          v.y = fma(dg0.y, xa.y, fma(cxp0.y, xar, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
+          u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
+          u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
+          // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
+          const double2 p0 = lds2a(na), p1 = lds2a(na + nx8);
+          v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
+          u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
+          if (act) sts2a(na, v);
+          if (up_ok) sts2a(na + nx8, u);
+          // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas)
+          if (push_lo0) stc2a(na + dlo, v);
+          if (push_hi0) stc2a(na + dhi, v);
+          if (push_hi1) stc2a(na + dhi, u);
         }
-        if (fix_r) {
-          xar = lds1a(ca + 16u);
-          xbr = lds1a(ca + nx8 + 16u);
-        }
-        double2 v, u;
-        v.x = fma(dg0.x, xa.x, fma(cxp0.x, xa.y, fma(cxm0, xal, fma(cyp0.x, xb.x, cym0.x * xd.x))));
-        v.y = fma(dg0.y, xa.y, fma(cxp0.y, xar, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
-        u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
-        u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
-        // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
-        const double2 p0 = REG ? ypa[cc] : lds2a(na), p1 = REG ? ypb[cc] : lds2a(na + nx8);
-        v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
-        u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
-        if (REG) {
-          ypa[cc] = xa;
-          ypb[cc] = xb;
-          ysa[cc] = v;
-          ysb[cc] = u;
-        }
-        if (act) sts2a(na, v);
-        if (up_ok) sts2a(na + nx8, u);
-        // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas)
-        if (push_lo0) stc2a(na + dlo, v);
-        if (push_hi0) stc2a(na + dhi, v);
-        if (push_hi1) stc2a(na + dhi, u);
-        acur[cc] = na;
-        anxt[cc] = ca;
       }
     }
-    cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc)                        // the buffers swap roles for every column stepped
+      if (st < mcol[cc]) {
+        const unsigned t = acur[cc];
+        acur[cc] = anxt[cc];
+        anxt[cc] = t;
+      }
+    if (!SPLIT) cluster_barrier();                         // nxt (and pushed ghosts) complete cluster-wide
+  }
+  if (SPLIT) {
+    __syncwarp();
+    cluster_barrier();                                     // last step's stores; no CTA exits while pushed to
   }
   for (int cc = 0; cc < ncb; ++cc) {
     const double* fin = cbuf + (size_t)(2 * cc + (mcol[cc] & 1)) * pitch;
@@ -1426,7 +1437,7 @@ static int g_res_attr = 0;
 // (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
 // clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
 int stencil_init_attrs();
-template <int CS, int CB, bool REG>
+template <int CS, int CB, bool SPLIT>
 __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
                             const int* __restrict__ deg);
@@ -1508,10 +1519,17 @@ bool filter_resident_ok(const scsf_ops* ops) {
   return filter_kind(ops) > 0;
 }
 
+// SCSF_FILTER_SPLIT = 1: the split-barrier variant of k_filter_cl (A/B; read per call: tests toggle it)
+static bool filter_split() {
+  const char* e = getenv("SCSF_FILTER_SPLIT");
+  return e && e[0] == '1';
+}
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
-  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  if (filter_split())
+    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, false>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 template <int CS>
 static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* cf, int64_t ldc, int nx, int ny,
@@ -1519,10 +1537,6 @@ static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* c
                                 const int* deg) {
   if (cb == 4) return launch_cl1<CS, 4>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   if (cb == 2) return launch_cl1<CS, 2>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-  if (cb == -2)                                            // register-resident patch rows, 2 columns
-    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, 2, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-  if (cb == -1)
-    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, 1, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
   return launch_cl1<CS, 1>(cfg, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 static cudaError_t launch_rp(cudaLaunchConfig_t& cfg, int cs, const double* cf, int64_t ldc, int nx, int ny,
@@ -1563,13 +1577,17 @@ static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-#define SCSF_CLR_ATTR(CS, CB) \
+#define SCSF_CLS_ATTR(CS, CB) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
-  SCSF_CLR_ATTR(1, 1); SCSF_CLR_ATTR(1, 2); SCSF_CLR_ATTR(2, 1); SCSF_CLR_ATTR(2, 2); SCSF_CLR_ATTR(4, 1);
-  SCSF_CLR_ATTR(4, 2); SCSF_CLR_ATTR(8, 1); SCSF_CLR_ATTR(8, 2); SCSF_CLR_ATTR(16, 1); SCSF_CLR_ATTR(16, 2);
+  SCSF_CLS_ATTR(1, 1); SCSF_CLS_ATTR(1, 2); SCSF_CLS_ATTR(1, 4);
+  SCSF_CLS_ATTR(2, 1); SCSF_CLS_ATTR(2, 2); SCSF_CLS_ATTR(2, 4);
+  SCSF_CLS_ATTR(4, 1); SCSF_CLS_ATTR(4, 2); SCSF_CLS_ATTR(4, 4);
+  SCSF_CLS_ATTR(8, 1); SCSF_CLS_ATTR(8, 2); SCSF_CLS_ATTR(8, 4);
+  SCSF_CLS_ATTR(16, 1); SCSF_CLS_ATTR(16, 2); SCSF_CLS_ATTR(16, 4);
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-#undef SCSF_CLR_ATTR
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#undef SCSF_CLS_ATTR
 #undef SCSF_CL_ATTR
 #define SCSF_RP_ATTR(CS) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_rp<CS, RP_CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
@@ -1586,13 +1604,6 @@ int stencil_init_attrs() {
   return status;
 }
 
-
-// SCSF_FILTER_REG = 1 / 2: the register-resident-rows variant of k_filter_cl with 2 / 1 columns per
-// CTA (A/B switch; default off)
-static int filter_reg_cols() {                            // read per call (tests toggle it)
-  const char* e = getenv("SCSF_FILTER_REG");
-  return (e && e[0] == '1') ? 2 : (e && e[0] == '2') ? 1 : 0;
-}
 
 // Whole filter (steps 0..m-1) for ncols columns of X into Out, column-resident kernel.
 int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* Out, int64_t ldv, int ncols,
@@ -1625,14 +1636,12 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
   } else if (cs > 0) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
-    int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
+    const int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
     const int thr = (int)round_up((int64_t)(R / 2) * (ops->nx / 2), 32);
-    const int regc = thr <= CL_T_REG ? filter_reg_cols() : 0;
-    if (regc > 0) cb = -min(cb, regc);                     // register-resident rows: 1 or 2 columns per CTA
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs, ceil_div(ncols, cb < 0 ? -cb : cb), 1);
+    cfg.gridDim = dim3(cs, ceil_div(ncols, cb), 1);
     cfg.blockDim = dim3(thr, 1, 1);
-    cfg.dynamicSmemBytes = per_col * (cb < 0 ? -cb : cb);
+    cfg.dynamicSmemBytes = per_col * cb;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

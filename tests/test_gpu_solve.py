@@ -39,12 +39,16 @@ def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
     f = synth.make_batch(cfg, 3)
     ops, _ = device_problem(f)
     coef = ops.coef.cpu().numpy()
+    eps = np.finfo(np.float64).eps
     for i in range(3):
         diag, offs = oop.stencil(f, i)
         n = f.n
-        assert np.allclose(coef[i, 0, :n], diag, rtol=1e-15, atol=0)
+        # diag = (sum of the 2d face coefficients) / h^2 + c: the two sides add the 2d + 1 positive
+        # terms in different orders, so they may differ by up to 2d rounding steps (2d eps relative);
+        # an off-diagonal is one product -a / h^2 on both sides (1 rounding step each: 2 eps)
+        assert np.allclose(coef[i, 0, :n], diag, rtol=2 * cfg.dim * eps, atol=0)
         for d, off in enumerate(offs):
-            assert np.allclose(coef[i, 1 + d, :n], off, rtol=1e-15, atol=0)
+            assert np.allclose(coef[i, 1 + d, :n], off, rtol=2 * eps, atol=0)
         assert np.all(coef[i, :, n:] == 0.0)
 
 
@@ -85,14 +89,15 @@ def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * scale)
 
 
-@pytest.mark.parametrize("reg", ["1", "2"])
+@pytest.mark.parametrize("split", ["0", "1"])
 @pytest.mark.parametrize("cfg_name,nx,k,m", [("C3", 200, 5, 20), ("C3", 190, 3, 9), ("C2", 100, 6, 20),
                                              ("C2", 92, 5, 20), ("C3", 76, 4, 9)])
-def test_filter_register_rows_variant(lib, cfg_name, nx, k, m, reg, monkeypatch):
-    """k_filter_cl with its patch rows of Y_s / Y_{s-1} held in registers (SCSF_FILTER_REG=1: 2 columns
-    per CTA, =2: 1), against the oracle, on 16-CTA (nx 190/200) and 8-CTA clusters with ragged slabs."""
+def test_filter_cluster_variants(lib, cfg_name, nx, k, m, split, monkeypatch):
+    """k_filter_cl against the oracle on 16-CTA (nx 190/200) and 8-CTA clusters with ragged slabs:
+    one full cluster barrier per step (default) or the split arrive / wait with the interior patches
+    in between (SCSF_FILTER_SPLIT=1)."""
     import torch
-    monkeypatch.setenv("SCSF_FILTER_REG", reg)
+    monkeypatch.setenv("SCSF_FILTER_SPLIT", split)
     monkeypatch.delenv("SCSF_FILTER_STREAMING", raising=False)
     cfg = synth.get_config(cfg_name).with_(nx=nx)
     f = synth.make_batch(cfg, 1)
@@ -226,6 +231,28 @@ def test_tiny_full_block_and_odd_sizes(lib):
     for L, nex, m in [(25, 0, 8), (7, 2, 1), (1, 1, 20), (1, 3, 5), (24, 1, 3)]:
         ev, vecs, st = lib.solve_one(ops, 0, L, nex, m, 1e-10, 500, seed=9)
         assert np.abs(ev.cpu().numpy()[:L] - w[:L]).max() <= 1e-9 * w[:L].max(), (L, nex, m)
+
+
+def test_no_extra_columns_is_reported_not_garbage(lib):
+    """nex = 0 with b = L < n: the damped interval [alpha, beta] starts at the L-th Ritz value itself
+    (reading R9), so that pair gains nothing per filter and the method need not converge.  The solve
+    must then end cleanly: SCSF_ERR_NUMERICAL or OK, finite outputs, and correct values when OK."""
+    f = synth.make_batch(synth.get_config("C1").with_(nx=12), 1)
+    ops, _ = device_problem(f)
+    w = np.linalg.eigvalsh(oop.assemble_dense(f, 0))
+    ev, vecs, st = lib.solve_one(ops, 0, 8, 0, 20, 1e-8, 60, seed=3, raise_on_fail=False)
+    e = ev.cpu().numpy()[:8]
+    assert st["status"] in (lib.SCSF_OK, lib.SCSF_ERR_NUMERICAL)
+    assert np.all(np.isfinite(e)) and bool(torch_isfinite(vecs))
+    if st["status"] == lib.SCSF_OK:
+        assert np.abs(e - w[:8]).max() <= 1e-9 * w[7]
+    else:
+        assert st["n_locked"] < 8 and st["iterations"] == 60
+
+
+def torch_isfinite(t):
+    import torch
+    return torch.isfinite(t).all()
 
 
 def test_max_iter_zero_reports_not_converged(lib):
