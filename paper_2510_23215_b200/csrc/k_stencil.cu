@@ -724,12 +724,7 @@ constexpr int CL_MAXP = CL_T;                    // 2 x 2 patches per CTA
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
-}
+
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
@@ -757,10 +752,7 @@ __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
-// SPLIT: the per-step cluster barrier is split into arrive / wait, and the patches that read no
-// ghost row (not in the slab's first or last row: they need only their own CTA's previous step)
-// run between the two, hiding the cluster-wide synchronisation behind most of the step's work.
-template <int CS, int CB, bool SPLIT = false>
+template <int CS, int CB>
 __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
@@ -867,21 +859,9 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
   const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
-  const bool bnd = (lr0 == 0) || (lr0 + 2 >= rows);        // reads a ghost row (SPLIT)
   for (int st = 0; st < mrun; ++st) {
     const double a = sa[st], bco = sb[st];
-    if (SPLIT && st > 0) {
-      __syncwarp();
-      cluster_arrive();                                    // my stores of step st - 1 (incl. DSMEM pushes)
-      __syncthreads();                                     // this CTA's stores of step st - 1 are visible
-    }
-#pragma unroll
-    for (int ph = 0; ph < (SPLIT ? 2 : 1); ++ph) {
-      if (SPLIT && ph == 1 && st > 0) {
-        __syncwarp();
-        cluster_wait();                                    // neighbours' ghost rows of step st - 1
-      }
-      if (SPLIT && ((ph == 0) == bnd)) continue;           // phase 0: interior patches, 1: boundary
+    {
 #pragma unroll
       for (int cc = 0; cc < CB; ++cc) {
         if (st < mcol[cc]) {                               // uniform across the CTA (0 beyond ncb)
@@ -925,11 +905,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         acur[cc] = anxt[cc];
         anxt[cc] = t;
       }
-    if (!SPLIT) cluster_barrier();                         // nxt (and pushed ghosts) complete cluster-wide
-  }
-  if (SPLIT) {
-    __syncwarp();
-    cluster_barrier();                                     // last step's stores; no CTA exits while pushed to
+    cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
   }
   for (int cc = 0; cc < ncb; ++cc) {
     const double* fin = cbuf + (size_t)(2 * cc + (mcol[cc] & 1)) * pitch;
@@ -1437,7 +1413,7 @@ static int g_res_attr = 0;
 // (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
 // clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
 int stencil_init_attrs();
-template <int CS, int CB, bool SPLIT>
+template <int CS, int CB>
 __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
                             const int* __restrict__ deg);
@@ -1519,17 +1495,10 @@ bool filter_resident_ok(const scsf_ops* ops) {
   return filter_kind(ops) > 0;
 }
 
-// SCSF_FILTER_SPLIT = 1: the split-barrier variant of k_filter_cl (A/B; read per call: tests toggle it)
-static bool filter_split() {
-  const char* e = getenv("SCSF_FILTER_SPLIT");
-  return e && e[0] == '1';
-}
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
-  if (filter_split())
-    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, false>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 template <int CS>
 static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* cf, int64_t ldc, int nx, int ny,
@@ -1577,17 +1546,7 @@ static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-#define SCSF_CLS_ATTR(CS, CB) \
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
-  SCSF_CLS_ATTR(1, 1); SCSF_CLS_ATTR(1, 2); SCSF_CLS_ATTR(1, 4);
-  SCSF_CLS_ATTR(2, 1); SCSF_CLS_ATTR(2, 2); SCSF_CLS_ATTR(2, 4);
-  SCSF_CLS_ATTR(4, 1); SCSF_CLS_ATTR(4, 2); SCSF_CLS_ATTR(4, 4);
-  SCSF_CLS_ATTR(8, 1); SCSF_CLS_ATTR(8, 2); SCSF_CLS_ATTR(8, 4);
-  SCSF_CLS_ATTR(16, 1); SCSF_CLS_ATTR(16, 2); SCSF_CLS_ATTR(16, 4);
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-#undef SCSF_CLS_ATTR
+
 #undef SCSF_CL_ATTR
 #define SCSF_RP_ATTR(CS) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_rp<CS, RP_CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
