@@ -58,7 +58,8 @@ def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
                                              ("C2", 40, 1, 1), ("C2", 100, 6, 20), ("C5", 110, 3, 5),
                                              ("C2", 92, 5, 20), ("C1", 132, 3, 20), ("C3", 76, 4, 9),
                                              ("C2", 124, 2, 3), ("C1", 30, 5, 20), ("C3", 34, 3, 7),
-                                             ("C3", 200, 5, 20), ("C3", 190, 3, 9)])
+                                             ("C3", 200, 5, 20), ("C3", 190, 3, 9), ("C4", 12, 5, 20),
+                                             ("C4", 40, 3, 7), ("C4", 20, 6, 9)])
 def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     """Both filter paths: resident (2-D: the register-patch kernel k_filter_rp when one CTA holds a
     column -- nx 30/32/34/40; 30 and 34 leave a 2-row top patch -- the cluster kernel with DSMEM
@@ -87,6 +88,32 @@ def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
     scale = np.abs(ref).max(axis=0)
     assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * scale)
+
+
+@pytest.mark.parametrize("z3", ["0", "1"])
+@pytest.mark.parametrize("nx,k,m", [(12, 3, 9), (40, 5, 20), (16, 2, 4), (44, 3, 6)])
+def test_filter_3d_zmarch_and_grouped(lib, nx, k, m, z3, monkeypatch):
+    """3-D streaming step: the z-marching kernel (k_stencil_z3, whole xy planes per CTA, 8-plane
+    z-chunks, ragged last chunk at nx = 12 / 44) and the grouped-load kernel (SCSF_Z3=0), against
+    the oracle."""
+    import torch
+    monkeypatch.setenv("SCSF_Z3", z3)
+    cfg = synth.get_config("C4").with_(nx=nx)
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    n, ld = f.n, ops.ld
+    Y0 = np.random.default_rng(nx).standard_normal((n, k))
+    A = oop.assemble_csr(f, 0)
+    normA = float(np.abs(A).sum(axis=1).max())
+    lam, alpha = 0.002 * normA, 0.1 * normA
+    c, e = (alpha + normA) / 2, (normA - alpha) / 2
+    Yd = torch.zeros((k, ld), dtype=torch.float64, device="cuda")
+    Yd[:, :n] = torch.from_numpy(Y0.T.copy())
+    Ym = _np_block(lib.cheb_filter(ops, 0, Yd, m, lam, c, e), n)
+    ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
+    assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * np.abs(ref).max(axis=0))
+    # the ld padding stays zero (it is read by later block products)
+    assert float(torch.abs(lib.cheb_filter(ops, 0, Yd, m, lam, c, e)[:, n:]).max() if ld > n else 0.0) == 0.0
 
 
 def test_filter_closed_form_laplacian(lib):
