@@ -693,136 +693,6 @@ __global__ void __launch_bounds__(PR * 4) k_gemm_nn3(const double* __restrict__ 
   }
 }
 
-// ---- NN for inner dimensions 257-368 (C5, b = 360): k_gemm_nn4.  k_gemm_nn3<32> holds a 32-row
-// panel (4 warps, one per SM sub-partition) and streams all of M past every 32 rows.  Here the
-// 64-row panel is stored without padding (64 x 368 doubles = 188 KB) with an XOR swizzle that keeps
-// the DMMA fragment loads conflict-free: element (k, r) sits at k * 64 + (r ^ 4 (k & 3)), so the 16
-// lanes of a 64-bit load phase (rows g, g = 0..3, k = t, t = 0..3) hit 16 distinct 8-byte bank
-// pairs.  M streams in chunks of 8 k-rows x 128 columns through a 3-stage cp.async ring (pitch 12:
-// 12 j + t is distinct mod 16), so 8 warps share each M chunk over 64 rows: twice the warps per SM
-// and half the M traffic per row of k_gemm_nn3<32>.  Out may alias X (the whole panel is staged
-// before the first write).
-constexpr int NN4_PR = 64, NN4_KC = 8, NN4_MP = 12, NN4_ST = 3, NN4_NT = 256;
-constexpr int NN4_MAX_K = 368;
-
-__global__ void __launch_bounds__(NN4_NT) k_gemm_nn4(const double* __restrict__ X, int64_t ldx, int64_t n, int b1,
-                                                   const double* __restrict__ M, int64_t ldm, int b2, double alpha,
-                                                   double beta, double* Out, int64_t ldo, int tri_upper, int a16) {
-  extern __shared__ __align__(16) double smd[];
-  const int b1r = (b1 + NN4_KC - 1) / NN4_KC * NN4_KC;
-  double* xp = smd;                                  // [b1r][64], swizzled rows
-  double* ms = smd + (size_t)b1r * NN4_PR;           // [NN4_ST][128][NN4_MP]
-  const int64_t r0 = (int64_t)blockIdx.x * NN4_PR;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;
-  const int nck_all = b1r / NN4_KC;
-  const int rows_here = (int)min((int64_t)NN4_PR, n - r0);
-
-  auto issue_panel = [&](int c) {                    // 8 k-columns x 64 rows: 256 16-byte segments
-    const int kk = tid >> 5, seg = tid & 31;
-    const int k = c * NN4_KC + kk;
-    const int rr = 2 * seg;
-    const int rem = (k < b1) ? max(0, min(2, rows_here - rr)) : 0;
-    const double* src = rem ? X + r0 + rr + (int64_t)k * ldx : X;
-    double* dst = xp + (size_t)k * NN4_PR + (rr ^ (4 * (k & 3)));
-    if (a16) {
-      cp_async16(dst, src, 8 * rem);
-    } else {
-      cp_async8(dst, src, rem ? 8 : 0);
-      cp_async8(dst + 1, rem > 1 ? src + 1 : src, rem > 1 ? 8 : 0);
-    }
-  };
-  auto issue_m = [&](int c, int j0, int stage) {   // 128 columns x 8 k: 1024 doubles (8-byte copies)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + NN4_NT * q;            // 0..1023
-      const int j = idx >> 3, kk = idx & 7;
-      const int k = c * NN4_KC + kk;
-      const bool ok = (k < b1) && (j0 + j < b2);
-      cp_async8(ms + ((size_t)stage * NN3_BN + j) * NN4_MP + kk,
-                ok ? (const void*)(M + k + (int64_t)(j0 + j) * ldm) : (const void*)M, ok ? 8 : 0);
-    }
-  };
-
-  for (int j0 = 0; j0 < b2; j0 += NN3_BN) {
-    const bool first = (j0 == 0);
-    const int nck = tri_upper ? min(nck_all, (min(b2, j0 + NN3_BN) + NN4_KC - 1) / NN4_KC) : nck_all;
-    const int ncp = first ? nck_all : 0;
-    double acc[4][4][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int c = 0; c < NN4_ST - 1; ++c) {
-      if (c < nck) {
-        issue_m(c, j0, c);
-        if (c < ncp) issue_panel(c);
-      }
-      cp_commit();
-    }
-    for (int c = 0; c < nck; ++c) {
-      cp_wait<NN4_ST - 2>();                          // chunk c landed (this thread's copies) ...
-      __syncthreads();                                // ... everyone's; stage (c + 2) % 3 is free
-      if (c + NN4_ST - 1 < nck) {
-        issue_m(c + NN4_ST - 1, j0, (c + NN4_ST - 1) % NN4_ST);
-        if (c + NN4_ST - 1 < ncp) issue_panel(c + NN4_ST - 1);
-      }
-      cp_commit();
-      const int stage = c % NN4_ST;
-      const bool idle = (j0 + wn >= b2) || (tri_upper && c * NN4_KC > j0 + wn + 31);
-      if (!idle) {
-#pragma unroll
-        for (int kk = 0; kk < NN4_KC; kk += 4) {
-          const int k = c * NN4_KC + kk + t;
-          const double* xa = xp + (size_t)k * NN4_PR;
-          const int sw = 4 * t;                      // 4 (k & 3), k = kk + t with kk % 4 == 0
-          double a[4], b[4];
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi) a[mi] = xa[(wm + mi * 8 + g) ^ sw];
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) b[ni] = ms[((size_t)stage * NN3_BN + wn + ni * 8 + g) * NN4_MP + kk + t];
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-        }
-      }
-    }
-    cp_wait<0>();
-    if (first && nck < ncp) {                        // triangular M cut the first pass short: finish the panel
-      for (int c = nck; c < ncp; ++c) issue_panel(c);
-      cp_commit();
-      cp_wait<0>();
-    }
-    __syncthreads();                                 // every warp is past its panel reads before anyone writes Out
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = r0 + wm + mi * 8 + g;
-          const int j = j0 + wn + ni * 8 + 2 * t + e;
-          if (r < n && j < b2) {
-            double* o = Out + r + (int64_t)j * ldo;
-            double v = alpha * acc[mi][ni][e];
-            if (beta != 0.0) v = fma(beta, *o, v);
-            *o = v;
-          }
-        }
-    __syncthreads();                                 // the M ring is reused by the next pass
-  }
-}
-static size_t nn4_smem(int b1) {
-  const int b1r = (b1 + NN4_KC - 1) / NN4_KC * NN4_KC;
-  return ((size_t)b1r * NN4_PR + (size_t)NN4_ST * NN3_BN * NN4_MP) * sizeof(double);
-}
-static int nn4_enabled() {                         // SCSF_NN4=0: k_gemm_nn3<32> for b1 > 256 (A/B)
-  const char* e = getenv("SCSF_NN4");
-  return (e && e[0] == '0') ? 0 : 1;
-}
-
 // A (b x b, ld) <- upper triangle mirrored into the strict lower triangle
 __global__ void k_symm_upper(double* __restrict__ A, int b, int64_t ld) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
@@ -879,8 +749,6 @@ int dense_init_attrs() {
                                        (int)nn3_smem(NN2_MAX_K, 64)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn3_smem(NN_MAX_K, 32)));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)nn4_smem(NN4_MAX_K)));
   g_nn_smem_set = 1;
   return SCSF_OK;
 }
@@ -991,10 +859,6 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
   if (b1 <= NN2_MAX_K && b1 > nn3_min_k() && b2 > V2_T) {
     k_gemm_nn3<64><<<ceil_div(n, 64), 256, nn3_smem(b1, 64), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
                                                                  tri, a16n, m16n);
-  } else if (b1 > NN2_MAX_K && b1 <= NN4_MAX_K && nn4_enabled()) {
-    const int a16 = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
-    k_gemm_nn4<<<ceil_div(n, NN4_PR), NN4_NT, nn4_smem(b1), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
-                                                                tri, a16);
   } else if (b1 > NN2_MAX_K && nn3_big()) {
     k_gemm_nn3<32><<<ceil_div(n, 32), 128, nn3_smem(b1, 32), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
                                                                  tri, a16n, m16n);

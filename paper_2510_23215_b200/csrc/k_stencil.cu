@@ -597,130 +597,6 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4g(
   }
 }
 
-// ---- 3-D streaming step by z-marching (k_stencil_z3).  A CTA owns whole xy planes (one thread
-// per 4-point x-quad, nx ny / 4 <= 512 threads) of ZB columns and marches up a chunk of zc planes.  Each
-// thread keeps Y_s at z-1, z, z+1 of its quad in registers (the z-neighbours never leave the
-// thread) and the loads of plane z+2 are issued a step ahead; the plane z goes through shared
-// memory (double-buffered) for the x- and y-neighbours.  Global traffic per point and column:
-// Y_s once (+ the chunk's two halo planes), Y_{s-1} once, Y_{s+1} once; the coefficients are read
-// once per point for the ZB columns of the CTA.  SURVEY §8(d): C4's 7-point filter step.
-constexpr int Z3_ZB = 1;                         // columns per CTA (2: 128 registers spill)
-template <int ZB>
-__global__ void __launch_bounds__(512) k_stencil_z3(
-    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int nz,
-    const double* __restrict__ X, const double* Xp, double* Out, int64_t ldv, int ncols,
-    const double* __restrict__ fp, int step, int zc, const int* __restrict__ deg) {
-  extern __shared__ __align__(32) double zpl[];            // [2][ZB][nx ny]
-  const int tid = threadIdx.x;
-  const int q = tid;                                       // quad index in the plane
-  const int sxy = nx * ny;
-  const int nq = sxy >> 2;
-  const int j0 = blockIdx.y * ZB;
-  const int nc = min(ZB, ncols - j0);
-  int jlo = 0;                                             // per-column degrees: finished columns first
-  if (deg)
-    while (jlo < nc && __ldg(deg + j0 + jlo) <= step) ++jlo;
-  if (jlo >= nc) return;                                   // (uniform across the CTA)
-  const int z0 = blockIdx.x * zc, z1 = min(nz, z0 + zc);
-  double a, b, c;
-  step_scalars(fp, step, a, b, c);
-  const bool ok = q < nq;
-  const int k0 = 4 * q;                                    // in-plane point index of the quad
-  const int x0 = k0 % nx, y0 = k0 / nx;
-  const bool hxl = x0 > 0, hxr = x0 + 4 < nx, hym = y0 > 0, hyp = y0 + 1 < ny;
-  const double4 z4 = make_double4(0, 0, 0, 0);
-  double4 ym_[ZB], yc_[ZB], yp_[ZB];                       // Y_s at z-1, z, z+1 (this quad)
-  const int64_t kz0 = (int64_t)z0 * sxy + k0;
-#pragma unroll
-  for (int cc = 0; cc < ZB; ++cc) {
-    ym_[cc] = yc_[cc] = yp_[cc] = z4;
-    if (ok && cc >= jlo && cc < nc) {
-      const double* x = X + (int64_t)(j0 + cc) * ldv;
-      if (z0 > 0) ym_[cc] = ldg4_nc(x + kz0 - sxy);
-      yc_[cc] = ldg4_nc(x + kz0);
-      if (z0 + 1 < nz) yp_[cc] = ldg4_nc(x + kz0 + sxy);
-    }
-  }
-  double4 czm = z4;                                        // cz of the plane below (A(k - sxy, k))
-  if (ok && z0 > 0) czm = ldg4_nc(cf + 3 * ldc + kz0 - sxy);
-  for (int z = z0; z < z1; ++z) {
-    const int64_t kz = (int64_t)z * sxy + k0;
-    // loads of this step issued first: coefficients of plane z, Y_{s-1}(z), Y_s(z+2)
-    double4 dg = z4, cxp = z4, cyp = z4, cym = z4, czp = z4;
-    double cxm = 0.0;
-    double4 pp[ZB], yn[ZB];
-    if (ok) {
-      dg = ldg4_nc(cf + kz);
-      cxp = ldg4_nc(cf + ldc + kz);
-      if (hxl) cxm = __ldg(cf + ldc + kz - 1);
-      cyp = ldg4_nc(cf + 2 * ldc + kz);
-      if (hym) cym = ldg4_nc(cf + 2 * ldc + kz - nx);
-      czp = ldg4_nc(cf + 3 * ldc + kz);
-    }
-#pragma unroll
-    for (int cc = 0; cc < ZB; ++cc) {
-      pp[cc] = z4;
-      yn[cc] = z4;
-      if (ok && cc >= jlo && cc < nc) {
-        if (b != 0.0) pp[cc] = ldg4_rd(Xp + (int64_t)(j0 + cc) * ldv + kz);
-        if (z + 2 < nz) yn[cc] = ldg4_nc(X + (int64_t)(j0 + cc) * ldv + kz + 2 * (int64_t)sxy);
-      }
-    }
-    // plane z of every column into shared memory (buffer z & 1) for the x / y neighbours
-    double* pl = zpl + (size_t)(z & 1) * ZB * sxy;
-#pragma unroll
-    for (int cc = 0; cc < ZB; ++cc)
-      if (ok) *reinterpret_cast<double4*>(pl + (size_t)cc * sxy + k0) = yc_[cc];
-    __syncthreads();
-#pragma unroll
-    for (int cc = 0; cc < ZB; ++cc) {
-      if (ok && cc >= jlo && cc < nc) {
-        const double* pc = pl + (size_t)cc * sxy;
-        const double4 xc = yc_[cc];
-        const double xl = hxl ? pc[k0 - 1] : 0.0;
-        const double xr = hxr ? pc[k0 + 4] : 0.0;
-        const double4 xu = hyp ? *reinterpret_cast<const double4*>(pc + k0 + nx) : z4;
-        const double4 xd = hym ? *reinterpret_cast<const double4*>(pc + k0 - nx) : z4;
-        const double4 zu = yp_[cc], zd = ym_[cc];
-        double4 v;
-        v.x = (dg.x - c) * xc.x + cxp.x * xc.y + cxm * xl + cyp.x * xu.x + cym.x * xd.x;
-        v.y = (dg.y - c) * xc.y + cxp.y * xc.z + cxp.x * xc.x + cyp.y * xu.y + cym.y * xd.y;
-        v.z = (dg.z - c) * xc.z + cxp.z * xc.w + cxp.y * xc.y + cyp.z * xu.z + cym.z * xd.z;
-        v.w = (dg.w - c) * xc.w + cxp.w * xr + cxp.z * xc.z + cyp.w * xu.w + cym.w * xd.w;
-        v.x += czp.x * zu.x + czm.x * zd.x;
-        v.y += czp.y * zu.y + czm.y * zd.y;
-        v.z += czp.z * zu.z + czm.z * zd.z;
-        v.w += czp.w * zu.w + czm.w * zd.w;
-        v.x *= a; v.y *= a; v.z *= a; v.w *= a;
-        if (b != 0.0) {
-          v.x = fma(b, pp[cc].x, v.x); v.y = fma(b, pp[cc].y, v.y); v.z = fma(b, pp[cc].z, v.z); v.w = fma(b, pp[cc].w, v.w);
-        }
-        stg4_nb(Out + (int64_t)(j0 + cc) * ldv + kz, v);
-      }
-      ym_[cc] = yc_[cc];
-      yc_[cc] = yp_[cc];
-      yp_[cc] = yn[cc];
-    }
-    czm = czp;
-  }
-  // ld padding (points n .. ldv) of the columns: the last z-chunk's CTA writes it
-  if (blockIdx.x == gridDim.x - 1) {
-    const int64_t n = (int64_t)sxy * nz;
-    for (int cc = jlo; cc < nc; ++cc)
-      for (int64_t k = n + tid; k < ldv; k += blockDim.x) Out[(int64_t)(j0 + cc) * ldv + k] = 0.0;
-  }
-}
-
-// Is the z-marching 3-D step usable (a CTA holds a plane: nx % 4 == 0, nx ny / 4 <= 512 threads,
-// 2 x ZB planes of shared memory)?  SCSF_Z3=0 keeps k_stencil_v4g for 3-D (read per call).
-static bool z3_ok(const scsf_ops* ops, int64_t ldv) {
-  const char* e = getenv("SCSF_Z3");
-  const bool on = !(e && e[0] == '0');
-  const int64_t sxy = (int64_t)ops->nx * ops->ny;
-  return on && ops->dim == 3 && ops->stencil == SCSF_STENCIL_FLUX && ops->nx % 4 == 0 && sxy / 4 <= 512 &&
-         (size_t)2 * Z3_ZB * sxy * sizeof(double) <= 200 * 1024 && ldv % 4 == 0 && ops->ld % 4 == 0;
-}
-
 // Columns whose loads are issued together.  Measured (tools/bench_filter.py, streaming filter at
 // m = 20, fraction of the measured HBM copy rate, plain k_stencil_v4 / G = 1 / 2 / 4):
 // C3 0.71 / 0.80 / 0.85 / 0.64, C4 (3-D) 0.51 / 0.66 / 0.53 / 0.48, C5 0.84 / 0.94 / 0.98 / 0.70
@@ -1660,7 +1536,6 @@ static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_res2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * RES_MAX_N * (int)sizeof(double)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_stencil_vib_t, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_stencil_z3<Z3_ZB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define SCSF_CL_ATTR(CS, CB) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
   SCSF_CL_ATTR(1, 1); SCSF_CL_ATTR(1, 2); SCSF_CL_ATTR(1, 4);
@@ -1774,18 +1649,6 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
     // the HBM peak with CB = 2 / 4: C3 0.74 / 0.75, C4 (3-D) 0.60 / 0.68, C5 0.85 / 0.88)
     constexpr int CB = 4;
     dim3 g(ceil_div(ceil_div(ldv, 4), SV_THREADS), ceil_div(ncols, CB));
-    if (ops->dim == 3 && z3_ok(ops, ldv)) {
-      SCSF_TRY(stencil_init_attrs());
-      const int sxy = ops->nx * ops->ny;
-      const char* ez = getenv("SCSF_Z3_ZC");              // planes per CTA (A/B; C4: 5 chunks of 40 planes)
-      const int zc = ez ? max(1, atoi(ez)) : 8;
-      dim3 g3(ceil_div(ops->nz, zc), ceil_div(ncols, Z3_ZB));
-      const int thr = (int)round_up(sxy / 4, 32);
-      k_stencil_z3<Z3_ZB><<<g3, thr, (size_t)2 * Z3_ZB * sxy * sizeof(double), s>>>(
-          cf, ops->ld, ops->nx, ops->ny, ops->nz, X, Xp, Out, ldv, ncols, fp, step, zc, deg);
-      SCSF_LAUNCH_CHECK();
-      return SCSF_OK;
-    }
     const int grp = v4_group(ops->dim);
 #define SCSF_V4G(D, G)                                                                                          \
   k_stencil_v4g<D, CB, G><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, \

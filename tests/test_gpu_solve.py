@@ -90,32 +90,6 @@ def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * scale)
 
 
-@pytest.mark.parametrize("z3", ["0", "1"])
-@pytest.mark.parametrize("nx,k,m", [(12, 3, 9), (40, 5, 20), (16, 2, 4), (44, 3, 6)])
-def test_filter_3d_zmarch_and_grouped(lib, nx, k, m, z3, monkeypatch):
-    """3-D streaming step: the z-marching kernel (k_stencil_z3, whole xy planes per CTA, 8-plane
-    z-chunks, ragged last chunk at nx = 12 / 44) and the grouped-load kernel (SCSF_Z3=0), against
-    the oracle."""
-    import torch
-    monkeypatch.setenv("SCSF_Z3", z3)
-    cfg = synth.get_config("C4").with_(nx=nx)
-    f = synth.make_batch(cfg, 1)
-    ops, _ = device_problem(f)
-    n, ld = f.n, ops.ld
-    Y0 = np.random.default_rng(nx).standard_normal((n, k))
-    A = oop.assemble_csr(f, 0)
-    normA = float(np.abs(A).sum(axis=1).max())
-    lam, alpha = 0.002 * normA, 0.1 * normA
-    c, e = (alpha + normA) / 2, (normA - alpha) / 2
-    Yd = torch.zeros((k, ld), dtype=torch.float64, device="cuda")
-    Yd[:, :n] = torch.from_numpy(Y0.T.copy())
-    Ym = _np_block(lib.cheb_filter(ops, 0, Yd, m, lam, c, e), n)
-    ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
-    assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * np.abs(ref).max(axis=0))
-    # the ld padding stays zero (it is read by later block products)
-    assert float(torch.abs(lib.cheb_filter(ops, 0, Yd, m, lam, c, e)[:, n:]).max() if ld > n else 0.0) == 0.0
-
-
 def test_filter_closed_form_laplacian(lib):
     import torch
     nx = 24
