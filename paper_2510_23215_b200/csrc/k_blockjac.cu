@@ -141,6 +141,9 @@ __device__ __forceinline__ int bj_orig(const BjPerm& arr, int i, int w, int b) {
 // Continues the sweep loop (DevLoop) while above tol and fewer than max_sweeps sweeps ran; a loop
 // that stops on the cap flags ctrl->nonfinite bit 2 (informational: the Rayleigh-Ritz rotation is
 // then exact but G not fully diagonal, so the residual test of l. 7 simply locks less).
+// COND: the kernel may set the WHILE node's condition (only the conditional-node mode needs that;
+// ncu does not profile, and the graph treats specially, kernels that can set a conditional handle)
+template <bool COND>
 __global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ Gp, int n, BjPerm arr, int w, int b,
                                                     double tol, int* __restrict__ counter, int max_sweeps,
                                                     Ctrl* ctrl, DevLoop loop) {
@@ -176,7 +179,10 @@ __global__ void __launch_bounds__(1024) k_bj_offmax(const double* __restrict__ G
     const bool above = v > tol;
     if (ctrl) ctrl->pad[0] += 1;                   // cumulative sweeps (stats)
     if (above && cnt >= max_sweeps && ctrl) atomicOr(&ctrl->nonfinite, 2);
-    dev_loop_continue(loop, above && cnt < max_sweeps);
+    if (COND)
+      dev_loop_continue(loop, above && cnt < max_sweeps);
+    else
+      *loop.flag = (above && cnt < max_sweeps) ? 1 : 0;
   }
 }
 
@@ -351,7 +357,10 @@ int blockjac_impl(const double* G, int64_t ldg, int b, double* scratch, double* 
         SCSF_LAUNCH_CHECK();
       }
     }
-    k_bj_offmax<<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, cap, ctrl, loop);
+    if (loop.in_graph)
+      k_bj_offmax<true><<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, cap, ctrl, loop);
+    else
+      k_bj_offmax<false><<<1, 1024, 0, bs>>>(Gp, n, A_last, w, b, 1e-14, counter_d, cap, ctrl, loop);
     SCSF_LAUNCH_CHECK();
     return SCSF_OK;
   };
