@@ -217,17 +217,17 @@ __global__ void __launch_bounds__(512) k_bj_final(const double* __restrict__ Gp,
   }
 }
 
-// SCSF_BJ_UNROLL=k (default 8): inside a CUDA-graph capture, run k unrolled sweeps whose kernels
+// SCSF_BJ_UNROLL=k (default 6): inside a CUDA-graph capture, run k unrolled sweeps whose kernels
 // return at once after convergence; 0: a WHILE conditional node instead.  Measured on C3 (64
-// operators, 32 chains, m = 60, tools/graph_ab.py): unrolled 2.10-2.14 s, eager with a host
+// operators, 32 chains, tools/graph_ab.py): m = 60: unrolled 2.10-2.14 s, eager with a host
 // synchronisation per sweep 2.31 s, conditional node 2.57 s (device-launched bodies of the 32
-// chains' graphs do not overlap as well); 8 sweeps never truncated a solve there (3.26 sweeps
-// per iteration on average, identical to the unbounded loop)
+// chains' graphs do not overlap as well); m = 120: unroll 4 / 5 / 6 / 8: 1.71 / 1.72 / 1.71 / 1.73 s,
+// and 6 sweeps never truncated a solve (3.58 sweeps per iteration, as the unbounded loop)
 static int bj_unroll() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SCSF_BJ_UNROLL");
-    v = e ? atoi(e) : 8;
+    v = e ? atoi(e) : 6;
     if (v < 0) v = 0;
   }
   return v;
