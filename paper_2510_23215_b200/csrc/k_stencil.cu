@@ -597,147 +597,6 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4g(
   }
 }
 
-// ---- 3-D streaming step with the CTA's coefficient tile staged in shared memory (k_stencil_v4s).
-// k_stencil_v4g<3> keeps a quad's 25 coefficient values in registers for its 4 columns (126
-// registers: 16 warps per SM, one column's loads in flight per thread).  Here the CTA first copies
-// the 512-point tile of the 6 coefficient streams it needs (diag, cx, cy, cz and the shifted cy, cz
-// of the neighbours below) into shared memory, and each column step reads them back from there, so
-// the registers hold only the loads of G columns: G = 1 at 7 CTAs per SM or G = 2 with two columns'
-// loads in flight.
-__device__ __forceinline__ double4 lds4v(const double* p) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  double4 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%4];\n\tld.shared.v2.f64 {%2, %3}, [%4+16];\n"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "r"(a));
-  return v;
-}
-template <int CB, int G>
-__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4s(
-    const double* __restrict__ cf, int64_t ldc, int nx, int ny, int64_t n,
-    const double* __restrict__ X, const double* Xp, double* Out,   // Out may alias Xp (same-index RMW)
-    int64_t ldv, int ncols, const double* __restrict__ fp, int step, const int* __restrict__ deg) {
-  constexpr int TP = 4 * SV_THREADS;                 // points per CTA
-  __shared__ __align__(32) double sc[6][TP];         // dg, cxp, cyp, cym, czp, czm of the tile
-  __shared__ double scxm[SV_THREADS];                // cx[k0 - 1] per quad
-  const int tid = threadIdx.x;
-  const int64_t kb = (int64_t)blockIdx.x * TP;
-  const int64_t k0 = kb + 4 * tid;
-  double a, b, c;
-  step_scalars(fp, step, a, b, c);
-  const int64_t sxy = (int64_t)nx * ny;
-  int j0 = blockIdx.y * CB;
-  const int j1 = min(ncols, j0 + CB);
-  if (deg)
-    while (j0 < j1 && __ldg(deg + j0) <= step) ++j0;
-  if (j0 >= j1) return;                              // (uniform across the CTA)
-  const double4 z4 = make_double4(0, 0, 0, 0);
-  // stage the coefficient tile (every thread one quad of each stream; zero outside the operator)
-  {
-    const bool in = k0 + 4 <= n;
-    const bool hym = k0 >= nx, hzm = k0 >= sxy;
-    double4 v0 = z4, v1 = z4, v2 = z4, v3 = z4, v4 = z4, v5 = z4;
-    double xm = 0.0;
-    if (in) {
-      v0 = ldg4_nc(cf + k0);
-      v1 = ldg4_nc(cf + ldc + k0);
-      v2 = ldg4_nc(cf + 2 * ldc + k0);
-      if (hym) v3 = ldg4_nc(cf + 2 * ldc + k0 - nx);
-      v4 = ldg4_nc(cf + 3 * ldc + k0);
-      if (hzm) v5 = ldg4_nc(cf + 3 * ldc + k0 - sxy);
-      if (k0 >= 1) xm = __ldg(cf + ldc + k0 - 1);
-    }
-    *reinterpret_cast<double4*>(&sc[0][4 * tid]) = v0;
-    *reinterpret_cast<double4*>(&sc[1][4 * tid]) = v1;
-    *reinterpret_cast<double4*>(&sc[2][4 * tid]) = v2;
-    *reinterpret_cast<double4*>(&sc[3][4 * tid]) = v3;
-    *reinterpret_cast<double4*>(&sc[4][4 * tid]) = v4;
-    *reinterpret_cast<double4*>(&sc[5][4 * tid]) = v5;
-    scxm[tid] = xm;
-  }
-  __syncthreads();
-  if (k0 >= ldv) return;
-  if (k0 + 4 > n) {                                  // tail quad / padding: scalar, guarded
-    for (int q = 0; q < 4; ++q) {
-      const int64_t k = k0 + q;
-      if (k >= ldv) break;
-      if (k >= n) {
-        for (int j = j0; j < j1; ++j) Out[(int64_t)j * ldv + k] = 0.0;
-        continue;
-      }
-      const double dgk = cf[k] - c;
-      const double xp = cf[ldc + k], xmk = (k >= 1) ? cf[ldc + k - 1] : 0.0;
-      const double yp = cf[2 * ldc + k], ym = (k >= nx) ? cf[2 * ldc + k - nx] : 0.0;
-      const double zp = cf[3 * ldc + k], zm = (k >= sxy) ? cf[3 * ldc + k - sxy] : 0.0;
-      for (int j = j0; j < j1; ++j) {
-        const double* x = X + (int64_t)j * ldv;
-        double v = dgk * x[k];
-        if (k + 1 < n) v = fma(xp, x[k + 1], v);
-        if (k >= 1) v = fma(xmk, x[k - 1], v);
-        if (k + nx < n) v = fma(yp, x[k + nx], v);
-        if (k >= nx) v = fma(ym, x[k - nx], v);
-        if (k + sxy < n) v = fma(zp, x[k + sxy], v);
-        if (k >= sxy) v = fma(zm, x[k - sxy], v);
-        v *= a;
-        if (b != 0.0) v = fma(b, Xp[(int64_t)j * ldv + k], v);
-        Out[(int64_t)j * ldv + k] = v;
-      }
-    }
-    return;
-  }
-  const bool hym = k0 >= nx, hyp = k0 + nx + 3 < n, hzm = k0 >= sxy, hzp = k0 + sxy + 3 < n;
-  const bool hm = k0 >= 1, hp = k0 + 4 < n;
-  const bool usep = b != 0.0;
-#pragma unroll
-  for (int g0 = 0; g0 < CB; g0 += G) {
-    double4 xc[G], xu[G], xd[G], zu[G], zd[G], pp[G];
-    double xl[G], xr[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q) {                    // every global load of the group first
-      const int j = j0 + g0 + q;
-      if (j < j1) {
-        const double* __restrict__ x = X + (int64_t)j * ldv;
-        xc[q] = ldg4_nc(x + k0);
-        xl[q] = hm ? __ldg(x + k0 - 1) : 0.0;
-        xr[q] = hp ? __ldg(x + k0 + 4) : 0.0;
-        xu[q] = hyp ? ldg4_nc(x + k0 + nx) : z4;
-        xd[q] = hym ? ldg4_nc(x + k0 - nx) : z4;
-        zu[q] = hzp ? ldg4_nc(x + k0 + sxy) : z4;
-        zd[q] = hzm ? ldg4_nc(x + k0 - sxy) : z4;
-        pp[q] = usep ? ldg4_rd(Xp + (int64_t)j * ldv + k0) : z4;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      const int j = j0 + g0 + q;
-      if (j < j1) {
-        // volatile shared loads: re-read per column (the compiler would otherwise hoist them into
-        // registers across the column loop, which is what this kernel avoids)
-        const double4 dg = lds4v(&sc[0][4 * tid]);
-        const double4 cxp = lds4v(&sc[1][4 * tid]);
-        const double4 cyp = lds4v(&sc[2][4 * tid]);
-        const double4 cym = lds4v(&sc[3][4 * tid]);
-        const double4 czp = lds4v(&sc[4][4 * tid]);
-        const double4 czm = lds4v(&sc[5][4 * tid]);
-        const double cxm = *(volatile const double*)&scxm[tid];
-        double4 v;
-        v.x = (dg.x - c) * xc[q].x + cxp.x * xc[q].y + cxm * xl[q] + cyp.x * xu[q].x + cym.x * xd[q].x;
-        v.y = (dg.y - c) * xc[q].y + cxp.y * xc[q].z + cxp.x * xc[q].x + cyp.y * xu[q].y + cym.y * xd[q].y;
-        v.z = (dg.z - c) * xc[q].z + cxp.z * xc[q].w + cxp.y * xc[q].y + cyp.z * xu[q].z + cym.z * xd[q].z;
-        v.w = (dg.w - c) * xc[q].w + cxp.w * xr[q] + cxp.z * xc[q].z + cyp.w * xu[q].w + cym.w * xd[q].w;
-        v.x += czp.x * zu[q].x + czm.x * zd[q].x;
-        v.y += czp.y * zu[q].y + czm.y * zd[q].y;
-        v.z += czp.z * zu[q].z + czm.z * zd[q].z;
-        v.w += czp.w * zu[q].w + czm.w * zd[q].w;
-        v.x *= a; v.y *= a; v.z *= a; v.w *= a;
-        if (usep) {
-          v.x = fma(b, pp[q].x, v.x); v.y = fma(b, pp[q].y, v.y); v.z = fma(b, pp[q].z, v.z); v.w = fma(b, pp[q].w, v.w);
-        }
-        stg4_nb(Out + (int64_t)j * ldv + k0, v);
-      }
-    }
-  }
-}
-
 // Columns whose loads are issued together.  Measured (tools/bench_filter.py, streaming filter at
 // m = 20, fraction of the measured HBM copy rate, plain k_stencil_v4 / G = 1 / 2 / 4):
 // C3 0.71 / 0.80 / 0.85 / 0.64, C4 (3-D) 0.51 / 0.66 / 0.53 / 0.48, C5 0.84 / 0.94 / 0.98 / 0.70
@@ -1794,15 +1653,7 @@ int stencil_impl(const scsf_ops* ops, int op, const double* X, const double* Xp,
 #define SCSF_V4G(D, G)                                                                                          \
   k_stencil_v4g<D, CB, G><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp, \
                                                    step, deg)
-    const char* es = getenv("SCSF_V4S");               // 3-D coefficient-staged step (A/B: 0 off, 1 / 2 = G)
-    const int v4s = (ops->dim == 3 && es) ? atoi(es) : 0;
-    if (v4s == 1) {
-      k_stencil_v4s<CB, 1><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp,
-                                                    step, deg);
-    } else if (v4s == 2) {
-      k_stencil_v4s<CB, 2><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, ops->nx, ops->ny, n, X, Xp, Out, ldv, ncols, fp,
-                                                    step, deg);
-    } else if (grp == 1) {
+    if (grp == 1) {
       if (ops->dim == 2) SCSF_V4G(2, 1); else SCSF_V4G(3, 1);
     } else if (grp == 2) {
       if (ops->dim == 2) SCSF_V4G(2, 2); else SCSF_V4G(3, 2);
