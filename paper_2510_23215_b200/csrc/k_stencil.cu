@@ -742,6 +742,33 @@ __device__ __forceinline__ double lds1a(unsigned a) {
 __device__ __forceinline__ void sts2a(unsigned a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// ---- tensor memory (TMEM) helpers (tcgen05; sm_100a).  A warp w reaches TMEM lanes
+// 32 (w % 4) .. 32 (w % 4) + 31; each lane is one thread, columns are 32-bit words.
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, double2& a, double2& b, double2& c, double2& d) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  auto d2 = [&](int i) { return __hiloint2double((int)r[i + 1], (int)r[i]); };
+  a = make_double2(d2(0), d2(2));
+  b = make_double2(d2(4), d2(6));
+  c = make_double2(d2(8), d2(10));
+  d = make_double2(d2(12), d2(14));
+}
+__device__ __forceinline__ void tmem_st8(unsigned taddr, double2 a, double2 b) {
+  const unsigned r0 = (unsigned)__double2loint(a.x), r1 = (unsigned)__double2hiint(a.x);
+  const unsigned r2 = (unsigned)__double2loint(a.y), r3 = (unsigned)__double2hiint(a.y);
+  const unsigned r4 = (unsigned)__double2loint(b.x), r5 = (unsigned)__double2hiint(b.x);
+  const unsigned r6 = (unsigned)__double2loint(b.y), r7 = (unsigned)__double2hiint(b.y);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+               "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(r4), "r"(r5), "r"(r6), "r"(r7)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 // distributed shared memory: 32-bit shared::cluster addresses (mapa) and stores
 __device__ __forceinline__ unsigned mapa32(unsigned a, unsigned rank) {
   unsigned r;
@@ -752,7 +779,11 @@ __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
-template <int CS, int CB>
+// TM: the thread's own patch rows of Y_s and Y_{s-1} live in tensor memory (two 8-word slots per
+// column, roles swapped every step) instead of being re-read from the shared buffers: per step and
+// column the shared-memory pipe serves only the rows below / above the patch, its stores and the
+// warp-edge x-neighbours (2 + edge loads instead of 6).
+template <int CS, int CB, bool TM = false>
 __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
@@ -859,6 +890,26 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
   const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
   cluster_barrier();                                       // also publishes sa / sb
+  __shared__ unsigned tm_base_s;
+  unsigned tbase = 0;                                      // this thread's TMEM address (lane, column 0)
+  if (TM) {
+    if ((tid >> 5) == 0) {
+      const unsigned sa32 = (unsigned)__cvta_generic_to_shared(&tm_base_s);
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(sa32) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int w = tid >> 5;
+    tbase = tm_base_s + ((unsigned)(32 * (w & 3)) << 16) + (unsigned)((w >> 2) * CB * 16);
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {                      // slot 0: Y_0 (own rows), slot 1: Y_{-1} = 0
+      tmem_st8(tbase + cc * 16, lds2a(acur[cc]), lds2a(acur[cc] + nx8));
+      tmem_st8(tbase + cc * 16 + 8, z2, z2);
+    }
+    tmem_wait_st();
+  }
   for (int st = 0; st < mrun; ++st) {
     const double a = sa[st], bco = sb[st];
     {
@@ -867,8 +918,21 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         if (st < mcol[cc]) {                               // uniform across the CTA (0 beyond ncb)
           const unsigned ca = acur[cc], na = anxt[cc];
           const double2 xd = lds2a(ca - nx8);
-          const double2 xa = lds2a(ca);
-          const double2 xb = lds2a(ca + nx8);
+          double2 xa, xb, p0, p1;
+          const unsigned tcur = tbase + cc * 16 + 8 * (st & 1), tprev = tbase + cc * 16 + 8 * ((st + 1) & 1);
+          if (TM) {
+            double2 q0, q1;
+            tmem_ld16(tbase + cc * 16, q0, q1, p0, p1);          // both slots: Y_s and Y_{s-1}
+            if (st & 1) {
+              xa = p0; xb = p1; p0 = q0; p1 = q1;
+            } else {
+              xa = q0; xb = q1;
+            }
+            if (!up_ok) xb = lds2a(ca + nx8);                    // no upper row: the ghost row above
+          } else {
+            xa = lds2a(ca);
+            xb = lds2a(ca + nx8);
+          }
           const double2 xu = lds2a(ca + up8);
           double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
           double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
@@ -886,7 +950,10 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
           u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
           u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
           // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
-          const double2 p0 = lds2a(na), p1 = lds2a(na + nx8);
+          if (!TM) {
+            p0 = lds2a(na);
+            p1 = lds2a(na + nx8);
+          }
           v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
           u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
           if (act) sts2a(na, v);
@@ -895,8 +962,11 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
           if (push_lo0) stc2a(na + dlo, v);
           if (push_hi0) stc2a(na + dhi, v);
           if (push_hi1) stc2a(na + dhi, u);
+          if (TM) tmem_st8(tprev, v, u);                         // Y_{s+1} replaces Y_{s-1}
+          (void)tcur;
         }
       }
+      if (TM) tmem_wait_st();
     }
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc)                        // the buffers swap roles for every column stepped
@@ -906,6 +976,13 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         anxt[cc] = t;
       }
     cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
+  }
+  if (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if ((tid >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm_base_s) : "memory");
   }
   for (int cc = 0; cc < ncb; ++cc) {
     const double* fin = cbuf + (size_t)(2 * cc + (mcol[cc] & 1)) * pitch;
@@ -1413,7 +1490,7 @@ static int g_res_attr = 0;
 // (tools/bench_configs.py C2, three interleaved runs each: 1441 / 1298 / 1454 with 4-CTA
 // clusters, 1457 / 1452 / 1456 operators/s with 8-CTA clusters).
 int stencil_init_attrs();
-template <int CS, int CB>
+template <int CS, int CB, bool TM>
 __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
                             const int* __restrict__ deg);
@@ -1495,10 +1572,21 @@ bool filter_resident_ok(const scsf_ops* ops) {
   return filter_kind(ops) > 0;
 }
 
+// The TMEM-backed variant of k_filter_cl for CTAs of >= 512 threads (C3's 16-CTA clusters: 704).
+// Measured (tools/bench_filter.py, tools/graph_ab.py, 32 chains): C3 step 32.8 -> 29.9 us, C3 64
+// operators 1.715 -> 1.590 s; C2 (350-thread CTAs) 5.14 -> 5.49 us and 0.66-0.69 -> 0.72 s, so small
+// CTAs keep the shared-memory form.  SCSF_FILTER_TMEM = 0 / 1 forces either (read per call).
+static bool filter_tmem(unsigned threads) {
+  const char* e = getenv("SCSF_FILTER_TMEM");
+  if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+  return threads >= 512;
+}
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
-  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  if (filter_tmem(cfg.blockDim.x))
+    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, false>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
 }
 template <int CS>
 static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* cf, int64_t ldc, int nx, int ny,
@@ -1547,6 +1635,17 @@ static int stencil_init_attrs_once() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 
+#define SCSF_CLT_ATTR(CS, CB) \
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<CS, CB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+  SCSF_CLT_ATTR(1, 1); SCSF_CLT_ATTR(1, 2); SCSF_CLT_ATTR(1, 4);
+  SCSF_CLT_ATTR(2, 1); SCSF_CLT_ATTR(2, 2); SCSF_CLT_ATTR(2, 4);
+  SCSF_CLT_ATTR(4, 1); SCSF_CLT_ATTR(4, 2); SCSF_CLT_ATTR(4, 4);
+  SCSF_CLT_ATTR(8, 1); SCSF_CLT_ATTR(8, 2); SCSF_CLT_ATTR(8, 4);
+  SCSF_CLT_ATTR(16, 1); SCSF_CLT_ATTR(16, 2); SCSF_CLT_ATTR(16, 4);
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_cl<16, 4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#undef SCSF_CLT_ATTR
 #undef SCSF_CL_ATTR
 #define SCSF_RP_ATTR(CS) \
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_filter_rp<CS, RP_CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))

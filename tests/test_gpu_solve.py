@@ -90,6 +90,31 @@ def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * scale)
 
 
+@pytest.mark.parametrize("cfg_name,nx,k,m", [("C3", 200, 5, 20), ("C3", 190, 3, 9), ("C2", 100, 6, 20),
+                                             ("C2", 92, 5, 21), ("C3", 76, 4, 9), ("C1", 132, 3, 20)])
+def test_filter_tmem_variant(lib, cfg_name, nx, k, m, monkeypatch):
+    """k_filter_cl with the patch rows of Y_s / Y_{s-1} in tensor memory (SCSF_FILTER_TMEM=1: tcgen05
+    alloc / st / ld / dealloc) against the oracle, on 16-CTA (nx 190/200) and 8-CTA clusters with ragged
+    slabs and odd / even degrees (the two TMEM slots swap roles every step)."""
+    import torch
+    monkeypatch.setenv("SCSF_FILTER_TMEM", "1")
+    monkeypatch.delenv("SCSF_FILTER_STREAMING", raising=False)
+    cfg = synth.get_config(cfg_name).with_(nx=nx)
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    n, ld = f.n, ops.ld
+    Y0 = np.random.default_rng(13).standard_normal((n, k))
+    A = oop.assemble_csr(f, 0)
+    normA = float(np.abs(A).sum(axis=1).max())
+    lam, alpha = 0.002 * normA, 0.1 * normA
+    c, e = (alpha + normA) / 2, (normA - alpha) / 2
+    Yd = torch.zeros((k, ld), dtype=torch.float64, device="cuda")
+    Yd[:, :n] = torch.from_numpy(Y0.T.copy())
+    Ym = _np_block(lib.cheb_filter(ops, 0, Yd, m, lam, c, e), n)
+    ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
+    assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * np.abs(ref).max(axis=0))
+
+
 def test_filter_closed_form_laplacian(lib):
     import torch
     nx = 24
