@@ -892,10 +892,15 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   cluster_barrier();                                       // also publishes sa / sb
   __shared__ unsigned tm_base_s;
   unsigned tbase = 0;                                      // this thread's TMEM address (lane, column 0)
+  // columns: CB x 16 words per warp of a lane quadrant, rounded up to a power of two >= 32 (a CTA
+  // takes only what it needs, so two CTAs of a small slab can share the SM's 512 columns)
+  unsigned tm_cols = 32;
+  while (tm_cols < (unsigned)(((nthr / 32 + 3) / 4) * CB * 16)) tm_cols <<= 1;
   if (TM) {
     if ((tid >> 5) == 0) {
       const unsigned sa32 = (unsigned)__cvta_generic_to_shared(&tm_base_s);
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(sa32) : "memory");
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa32), "r"(tm_cols)
+                   : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -982,7 +987,8 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     if ((tid >> 5) == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm_base_s) : "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm_base_s), "r"(tm_cols)
+                   : "memory");
   }
   for (int cc = 0; cc < ncb; ++cc) {
     const double* fin = cbuf + (size_t)(2 * cc + (mcol[cc] & 1)) * pitch;
@@ -1572,14 +1578,15 @@ bool filter_resident_ok(const scsf_ops* ops) {
   return filter_kind(ops) > 0;
 }
 
-// The TMEM-backed variant of k_filter_cl for CTAs of >= 512 threads (C3's 16-CTA clusters: 704).
-// Measured (tools/bench_filter.py, tools/graph_ab.py, 32 chains): C3 step 32.8 -> 29.9 us, C3 64
-// operators 1.715 -> 1.590 s; C2 (350-thread CTAs) 5.14 -> 5.49 us and 0.66-0.69 -> 0.72 s, so small
-// CTAs keep the shared-memory form.  SCSF_FILTER_TMEM = 0 / 1 forces either (read per call).
+// The TMEM-backed variant of k_filter_cl is the default.  Measured (tools/bench_filter.py,
+// tools/graph_ab.py, 32 chains, profiles/r02_tmem_ab.json): C3 step 32.8 -> 29.9 us, C3 64 operators
+// 1.714 -> 1.585 s; C2 0.665-0.704 -> 0.652 s (with the allocation sized to the CTA, so two C2
+// CTAs share an SM's 512 columns; a fixed 512-column allocation made C2 7 % slower).
+// SCSF_FILTER_TMEM = 0 restores the shared-memory form (read per call).
 static bool filter_tmem(unsigned threads) {
+  (void)threads;
   const char* e = getenv("SCSF_FILTER_TMEM");
-  if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
-  return threads >= 512;
+  return !(e && e[0] == '0');
 }
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
