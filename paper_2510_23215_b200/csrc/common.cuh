@@ -10,7 +10,7 @@
 namespace scsf {
 
 // filter parameter block: {lambda, c, e, -} then the per-step (a_s, b_s) table (k_step_table)
-constexpr int FP_TAB = 4, FP_MAX_DEGREE = 128, FP_DOUBLES = FP_TAB + 2 * FP_MAX_DEGREE;
+constexpr int FP_TAB = 4, FP_MAX_DEGREE = 256, FP_DOUBLES = FP_TAB + 2 * FP_MAX_DEGREE;
 
 // coefficient arrays per operator (include/scsf.h stencil kinds)
 inline int ncoef(const scsf_ops* o) { return o->stencil == SCSF_STENCIL_VIB13 ? 7 : 1 + o->dim; }

@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
                                                        const int* __restrict__ deg) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
-  __shared__ double sa[128], sb[128];                      // per-step scalars (m <= 128)
+  __shared__ double sa[FP_MAX_DEGREE], sb[FP_MAX_DEGREE]; // per-step scalars (m <= FP_MAX_DEGREE)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     double sig = s1;
     sa[0] = s1 / e;
     sb[0] = 0.0;
-    for (int st = 1; st < m && st < 128; ++st) {
+    for (int st = 1; st < m && st < FP_MAX_DEGREE; ++st) {
       const double sn = 1.0 / (2.0 / s1 - sig);
       sa[st] = 2.0 * sn / e;
       sb[st] = -sn * sig;
@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict_
                                                        const int* __restrict__ deg) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
-  __shared__ double sa[128], sb[128];
+  __shared__ double sa[FP_MAX_DEGREE], sb[FP_MAX_DEGREE];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict_
     double sig = s1;
     sa[0] = s1 / e;
     sb[0] = 0.0;
-    for (int st = 1; st < m && st < 128; ++st) {
+    for (int st = 1; st < m && st < FP_MAX_DEGREE; ++st) {
       const double sn = 1.0 / (2.0 / s1 - sig);
       sa[st] = 2.0 * sn / e;
       sb[st] = -sn * sig;

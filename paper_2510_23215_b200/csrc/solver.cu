@@ -150,11 +150,16 @@ int carve_solve_ws(const scsf_ops* ops, int L, int nex, void* ws, size_t ws_byte
 // tile launch of an iteration, summed after the iteration's control-block read; the flops are
 // the algorithmic ones of the product (upper-triangle Grams count their unique entries)
 static int g_timing = 0;
+// kinds: 0 Gram (gram(): BCGS V_L^T F, CholQR Y^T Y), 1 triangular R^{-1} apply, 2 rotation (V Z, W Z),
+// 3 dual Gram [Q1^T Q1 | Q1^T W1], 4 V <- Q1 M, 5 BCGS update F -= V_L C
+constexpr int GT_KINDS = 6;
 struct GemmTiming {
   std::vector<cudaEvent_t> ev;     // pairs (begin, end), reused
   std::vector<double> flops;
+  std::vector<int> kind;
   size_t used = 0;
   double ms = 0.0, total_flops = 0.0;
+  double kind_ms[GT_KINDS] = {0}, kind_flops[GT_KINDS] = {0};
 };
 static thread_local GemmTiming* t_gt = nullptr;
 static int gt_begin(cudaStream_t s) {
@@ -170,12 +175,16 @@ static int gt_begin(cudaStream_t s) {
   SCSF_CUDA_CHECK(cudaEventRecord(g->ev[g->used], s));
   return SCSF_OK;
 }
-static int gt_end(cudaStream_t s, double flops) {
+static int gt_end(cudaStream_t s, double flops, int kind) {
   GemmTiming* g = t_gt;
   if (!g) return SCSF_OK;
   SCSF_CUDA_CHECK(cudaEventRecord(g->ev[g->used + 1], s));
-  if (g->flops.size() < g->ev.size() / 2) g->flops.resize(g->ev.size() / 2);
+  if (g->flops.size() < g->ev.size() / 2) {
+    g->flops.resize(g->ev.size() / 2);
+    g->kind.resize(g->ev.size() / 2);
+  }
   g->flops[g->used / 2] = flops;
+  g->kind[g->used / 2] = kind;
   g->used += 2;
   return SCSF_OK;
 }
@@ -188,6 +197,8 @@ static int gt_collect() {
     SCSF_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev[i], g->ev[i + 1]));
     g->ms += ms;
     g->total_flops += g->flops[i / 2];
+    g->kind_ms[g->kind[i / 2]] += ms;
+    g->kind_flops[g->kind[i / 2]] += g->flops[i / 2];
   }
   g->used = 0;
   return SCSF_OK;
@@ -199,7 +210,7 @@ static int gram(SolveWS& w, const double* X, int b1, const double* Y, int b2, in
                 cudaStream_t s) {
   SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_tn(X, w.ldv, b1, Y, w.ldv, b2, w.n, 1.0, sym, C, b1, w.P, s));
-  SCSF_TRY(gt_end(s, sym ? (double)w.n * b1 * (b1 + 1) : 2.0 * w.n * b1 * b2));
+  SCSF_TRY(gt_end(s, sym ? (double)w.n * b1 * (b1 + 1) : 2.0 * w.n * b1 * b2, 0));
   if (w.comm) SCSF_TRY(w.comm->allreduce_sum(C, (size_t)b1 * b2, s));
   return SCSF_OK;
 }
@@ -259,7 +270,7 @@ static int cholqr_pass(SolveWS& w, double* Y, double* Out, int ncols, cudaStream
   SCSF_TRY(chol_inv_impl(w.S, ncols, ncols, w.n_glob, w.Rinv, w.Gwork, w.ctrl, s));
   SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn_ex(Y, w.ldv, w.n, ncols, w.Rinv, ncols, ncols, 1.0, 0.0, Out, w.ldv, 1, s));
-  SCSF_TRY(gt_end(s, (double)w.n * ncols * (ncols + 1)));                     // triangular R^{-1}
+  SCSF_TRY(gt_end(s, (double)w.n * ncols * (ncols + 1), 1));                  // triangular R^{-1}
   return SCSF_OK;
 }
 
@@ -277,7 +288,7 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
   SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Va, w.ldv, s));
   SCSF_TRY(gemm_nn(Wa, w.ldv, w.n, ba, w.Zs, ba, ba, 1.0, 0.0, Wa, w.ldv, s));
-  SCSF_TRY(gt_end(s, 4.0 * w.n * ba * ba));
+  SCSF_TRY(gt_end(s, 4.0 * w.n * ba * ba, 2));
   SCSF_TRY(resid_impl(Va, Wa, w.ldv, w.n, ba, w.theta + k0, w.res + k0, w.wn + k0, s));
   if (w.comm) {
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
@@ -312,7 +323,7 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(spmm(ops, op, w, Va, nullptr, Wa, ba, -1, s));
   SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_tn_dual(Va, w.ldv, Va, Wa, w.ldv, ba, w.n, w.C2, ba, w.P, s));
-  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * (ba + 1)));                               // two upper Grams
+  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * (ba + 1), 3));                            // two upper Grams
   if (w.comm) SCSF_TRY(w.comm->allreduce_sum(w.C2, (size_t)2 * bb, s));
   const double* S2 = w.C2;
   double* H = w.C2 + bb;
@@ -324,7 +335,7 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
   SCSF_TRY(gemm_nn_ex(w.Rinv, ba, ba, ba, w.Zs, ba, ba, 1.0, 0.0, w.Mb, ba, 0, s));        // M = R2^{-1} Z
   SCSF_TRY(gt_begin(s));
   SCSF_TRY(gemm_nn(Va, w.ldv, w.n, ba, w.Mb, ba, ba, 1.0, 0.0, Va, w.ldv, s));
-  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * ba));
+  SCSF_TRY(gt_end(s, 2.0 * w.n * ba * ba, 4));
   // residuals of A V by one stencil pass (cheaper than the n x b x b product W1 M); without a row
   // partition the pass is fused with the norms and W is not written (only the residuals use it)
   bool fused = false;
@@ -551,6 +562,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
   static thread_local GemmTiming t_gt_store;
   t_gt_store.ms = 0.0;
   t_gt_store.total_flops = 0.0;
+  for (int k = 0; k < GT_KINDS; ++k) t_gt_store.kind_ms[k] = t_gt_store.kind_flops[k] = 0.0;
   t_gt_store.used = 0;
   t_gt = tm.on ? &t_gt_store : nullptr;
   Ctrl h{};
@@ -605,7 +617,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
         SCSF_TRY(gram(w, w.V, kLc, F, ba, 0, w.C, s));
         SCSF_TRY(gt_begin(s));
         SCSF_TRY(gemm_nn(w.V, w.ldv, w.n, kLc, w.C, kLc, ba, -1.0, 1.0, F, w.ldv, s));
-        SCSF_TRY(gt_end(s, 2.0 * w.n * kLc * ba));
+        SCSF_TRY(gt_end(s, 2.0 * w.n * kLc * ba, 5));
       }
     }
     // 3. CholQR, first pass (lands the block in V's active columns)
@@ -705,6 +717,12 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
     SCSF_TRY(gt_collect());
     st->t_gemm_ms = t_gt ? t_gt->ms : 0.0;
     st->gemm_flops = t_gt ? t_gt->total_flops : 0.0;
+    if (t_gt && getenv("SCSF_GEMM_PROFILE")) {          // per-kind DGEMM times (tools/; stderr)
+      fprintf(stderr, "scsf_gemm_profile n=%lld b=%d", (long long)w.n, b);
+      for (int k = 0; k < GT_KINDS; ++k)
+        fprintf(stderr, " k%d=%.4f/%.6e", k, t_gt->kind_ms[k], t_gt->kind_flops[k]);
+      fprintf(stderr, "\n");
+    }
   }
   if (status != SCSF_OK)
     set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op,

@@ -59,7 +59,8 @@ def test_assemble_matches_oracle_stencil(lib, cfg_name, nx):
                                              ("C2", 92, 5, 20), ("C1", 132, 3, 20), ("C3", 76, 4, 9),
                                              ("C2", 124, 2, 3), ("C1", 30, 5, 20), ("C3", 34, 3, 7),
                                              ("C3", 200, 5, 20), ("C3", 190, 3, 9), ("C4", 12, 5, 20),
-                                             ("C4", 40, 3, 7), ("C4", 20, 6, 9)])
+                                             ("C4", 40, 3, 7), ("C4", 20, 6, 9), ("C3", 200, 3, 150),
+                                             ("C2", 100, 4, 256), ("C4", 20, 2, 201)])
 def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
     """Both filter paths: resident (2-D: the register-patch kernel k_filter_rp when one CTA holds a
     column -- nx 30/32/34/40; 30 and 34 leave a 2-row top patch -- the cluster kernel with DSMEM
@@ -270,7 +271,7 @@ def test_bad_arguments(lib):
     f = synth.make_batch(synth.get_config("C1").with_(nx=6), 1)
     ops, _ = device_problem(f)
     for L, nex, m, tol in [(0, 1, 20, 1e-8), (30, 10, 20, 1e-8), (4, 1, 0, 1e-8), (4, 1, 20, 0.0), (4, 1, -3, 1e-8),
-                           (4, 1, 129, 1e-8), (4, 1, -129, 1e-8)]:
+                           (4, 1, 257, 1e-8), (4, 1, -257, 1e-8)]:
         with pytest.raises(lib.ScsfError) as ei:
             lib.solve_one(ops, 0, L, nex, m, tol, 10)
         assert ei.value.code == lib.SCSF_ERR_ARG
