@@ -46,7 +46,10 @@ CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 # filter sits in its slow regime and the outer iterations are 4-10x those of m = 60-120 (DESIGN.md
 # reading R27, tools/degree_sweep.py, profiles/r02_degree_sweep*.jsonl).  Every operator still
 # converges to the same tolerance; the line also reports the paper's m = 20 on the same queue.
-BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 120, "C4": 80, "C5": 80}
+# The degree has a stability ceiling: the filtered block's condition number grows like
+# exp(2 m sqrt(delta)) and CholQR squares it; on C3, m = 224 / 256 left 53 / 130 of 400 operators
+# unconverged (CholQR breakdown, profiles/r02_degree_limit_C3.jsonl), m = 160 / 192 none.
+BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 160, "C4": 80, "C5": 80}
 DEFAULT_CONFIG = "C3"
 
 
