@@ -99,7 +99,9 @@ typedef struct {
   double t_rr_ms;            /* Rayleigh-Ritz + residuals + locking (ll. 5-7)          */
   double filter_bytes;       /* algorithmic HBM bytes of the filter steps */
   int32_t jacobi_sweeps;     /* reduced-eigensolver sweeps, summed over RR steps      */
-  int32_t reserved0;
+  int32_t cold_retry;        /* 1 if a warm start broke down and the operator was     */
+                             /* solved again from a random block (R29); the counts    */
+                             /* above include both attempts                           */
   double t_gemm_ms;          /* tall-skinny DGEMM tiles (Gram / projection / rotation),
                                 CUDA events around each launch (0 unless timing is on)  */
   double gemm_flops;         /* their algorithmic flops (upper-triangle Grams: unique
@@ -229,6 +231,12 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  *            Honoured by the resident filters and the vectorised streaming step
  *            (5-/7-point operators, nx % 4 == 0); elsewhere (13-point family, row
  *            partition) it falls back to the uniform degree |m|.
+ *            Conditioning guard (R28): each filter runs at most the degree
+ *            for which C_m(t_lambda) = cosh(m acosh|(lambda - c)/e|) <= 1e8 (rounded
+ *            down to = m mod 3, >= 4), so a degree past CholQR's stability ceiling
+ *            is lowered on the device instead of breaking the orthonormalisation;
+ *            below that ceiling m is used as given.  stats->filter_steps counts
+ *            the steps actually run.
  *  max_iter  outer-iteration cap (R24; 200)
  *  warm_vecs dev [b][ld_vec] or NULL: initial block V~_0 ("V~_0 = V^(i-1)");
  *            NULL = seeded Gaussian start (R17), seed + op_index.

@@ -370,11 +370,35 @@ static int run_chain(const scsf_ops* ops, const int32_t* chain, int32_t n_chain,
   };
   const int r = [&]() -> int {
   int worst = SCSF_OK;
+  bool prev_ok = state_in != nullptr;      // a warm start needs a converged block to start from
   for (int k = 0; k < n_chain; ++k) {
     scsf_stats local{};
-    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, k > 0 || state_in != nullptr, false,
-                       seed + (uint64_t)chain[k], w, &local, s);
+    const bool warm = k > 0 ? prev_ok : state_in != nullptr;
+    int r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, warm, false, seed + (uint64_t)chain[k], w,
+                       &local, s);
+    if (r == SCSF_ERR_NUMERICAL && warm) {
+      // R29: a warm start that broke down (a queue neighbour too dissimilar for the inherited
+      // bounds, or a degree past the stability ceiling) is solved again from a random block, and
+      // the chain goes on from that result; the statistics count both attempts
+      scsf_stats again{};
+      r = solve_core(ops, chain[k], L, nex, degree, tol, max_iter, false, false, seed + (uint64_t)chain[k], w,
+                     &again, s);
+      again.iterations += local.iterations;
+      again.filter_steps += local.filter_steps;
+      again.cholqr_fallbacks += local.cholqr_fallbacks;
+      again.spmm_columns += local.spmm_columns;
+      again.t_filter_ms += local.t_filter_ms;
+      again.t_ortho_ms += local.t_ortho_ms;
+      again.t_rr_ms += local.t_rr_ms;
+      again.filter_bytes += local.filter_bytes;
+      again.jacobi_sweeps += local.jacobi_sweeps;
+      again.t_gemm_ms += local.t_gemm_ms;
+      again.gemm_flops += local.gemm_flops;
+      again.cold_retry = 1;
+      local = again;
+    }
     if (r != SCSF_OK && r != SCSF_ERR_NUMERICAL) return r;
+    prev_ok = (r == SCSF_OK);
     if (r > worst) worst = r;
     if (st) st[k] = local;
     if (evals)

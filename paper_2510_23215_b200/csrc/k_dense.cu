@@ -416,10 +416,11 @@ static int tma_encode_fn() {
   if (status != SCSF_OK) set_error("cuTensorMapEncodeTiled is not available from the driver");
   return status;
 }
-static int make_tmap(CUtensorMap* m, const double* X, int64_t ld, int64_t n, int cols) {
+static int make_tmap(CUtensorMap* m, const double* X, int64_t ld, int64_t n, int cols, int box_r = TNT_BOX_R,
+                     int box_c = V2_T) {
   cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)cols};
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-  cuuint32_t box[2] = {TNT_BOX_R, V2_T};
+  cuuint32_t box[2] = {(cuuint32_t)box_r, (cuuint32_t)box_c};
   cuuint32_t es[2] = {1, 1};
   const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -439,10 +440,20 @@ static bool tn_tma_enabled() {
   }
   return v == 1;
 }
-// TMA needs 16-byte aligned bases and leading dimensions (ld even) and row counts >= 16 to pay
-static bool tma_ok(const double* p, int64_t ld, int64_t n) {
-  return tn_tma_enabled() && ((uintptr_t)p & 15) == 0 && (ld & 1) == 0 && n >= 64 && n < (1ll << 31);
+// SCSF_NN_TMA=0 keeps k_gemm_nn3 for the wide NN products (A/B runs)
+static bool nn_tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_NN_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
+// TMA needs 16-byte aligned bases and leading dimensions (ld even) and row counts >= 16 to pay
+static bool tma_layout_ok(const double* p, int64_t ld, int64_t n) {
+  return ((uintptr_t)p & 15) == 0 && (ld & 1) == 0 && n >= 64 && n < (1ll << 31);
+}
+static bool tma_ok(const double* p, int64_t ld, int64_t n) { return tn_tma_enabled() && tma_layout_ok(p, ld, n); }
 
 // ---- NN: Out[r0:r0+64, :] = alpha X[r0:r0+64, 0:b1] M + beta Out.  The whole
 // 64-row panel of X stays resident (so Out may alias X); M streams through a
@@ -693,6 +704,135 @@ __global__ void __launch_bounds__(PR * 4) k_gemm_nn3(const double* __restrict__ 
   }
 }
 
+// ---- NN, TMA-fed, whole rows: Out[r0:r0+32, 0:b2] = alpha X[r0:r0+32, 0:b1] M + beta Out.
+// One producer warp streams k-chunks of 16 through an NNT_ST-stage mbarrier ring with
+// cp.async.bulk.tensor.2d (128-byte swizzle; zero fill past n, b1 and b2): two 16-row x 16-k boxes
+// of X and b2/128 16-k x 128-column boxes of M per chunk.  Eight consumer warps own 8*NI columns
+// each over the CTA's 32 rows (4 x NI DMMA blocks, 8 NI accumulators per lane), so every output
+// element is final when the chunk loop ends and the CTA writes whole rows: Out may alias X (all
+// of the CTA's X rows are in shared memory before any warp passes the last full barrier).
+//
+// Fragment maps (conflict-free 128-byte phases, as k_gemm_tn_tma): a 16-byte unit of an M line
+// holds k pair (kk + 2t, kk + 2t + 1) of one column; fragment column g of block ni is column
+// 8 ni + perm(g), perm(g) = (g >> 1) | ((g & 1) << 2), so the two columns of a phase (g, g + 1)
+// differ in bit 2 and their swizzled units (u ^ (col & 7)) never collide.  X is read one double
+// per lane: row 8 mi + g of the 32, k = kk + 2t (+1); 16 lanes cover 8 distinct 8-byte slots
+// pairs of all 32 banks.
+constexpr int NNT_BM = 32, NNT_KC = 16, NNT_CONS = 8, NNT_NT = (NNT_CONS + 1) * 32;
+constexpr int NNT_XBOX_BYTES = 16 * NNT_KC * 8;                 // 2 KB: 16 rows x 16 k
+constexpr int NNT_MBOX_COLS = 128, NNT_MBOX_BYTES = NNT_MBOX_COLS * NNT_KC * 8;   // 16 KB
+
+__host__ __device__ constexpr int nnt_stages(int NI) { return NI > 4 ? 4 : 6; }
+__host__ __device__ constexpr int nnt_mboxes(int NI) { return (NNT_CONS * 8 * NI + NNT_MBOX_COLS - 1) / NNT_MBOX_COLS; }
+__host__ __device__ constexpr int nnt_stage_bytes(int NI) { return 2 * NNT_XBOX_BYTES + nnt_mboxes(NI) * NNT_MBOX_BYTES; }
+
+template <int NI>
+__global__ void __launch_bounds__(NNT_NT, 1) k_gemm_nn_tma(const __grid_constant__ CUtensorMap tmX,
+                                                         const __grid_constant__ CUtensorMap tmM, int64_t n,
+                                                         int b1, int b2, double alpha, double beta,
+                                                         double* Out, int64_t ldo, int tri_upper) {
+  constexpr int ST = nnt_stages(NI), SB = nnt_stage_bytes(NI), NMB = nnt_mboxes(NI);
+  extern __shared__ __align__(1024) unsigned char nsm[];
+  unsigned char* base = nsm + ((1024 - (smem_u32(nsm) & 1023)) & 1023);
+  const uint32_t ring = smem_u32(base);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + ST * SB);
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * ST;
+  const int64_t r0 = (int64_t)blockIdx.x * NNT_BM;
+  const int nck = (b1 + NNT_KC - 1) / NNT_KC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) {
+      mbar_init(full0 + 8 * st, 1);
+      mbar_init(empty0 + 8 * st, NNT_CONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NNT_CONS) {                            // producer
+    if (lane == 0) {
+      const int nmb = min(NMB, (b2 + NNT_MBOX_COLS - 1) / NNT_MBOX_COLS);
+      for (int c = 0; c < nck; ++c) {
+        const int st = c % ST;
+        if (c >= ST) mbar_wait(empty0 + 8 * st, ((c / ST) - 1) & 1);
+        const uint32_t fb = full0 + 8 * st, dst = ring + st * SB;
+        mbar_expect_tx(fb, 2 * NNT_XBOX_BYTES + nmb * NNT_MBOX_BYTES);
+        const int k0 = c * NNT_KC;
+        tma_load_2d(dst, &tmX, (int)r0, k0, fb);
+        tma_load_2d(dst + NNT_XBOX_BYTES, &tmX, (int)r0 + 16, k0, fb);
+        for (int q = 0; q < nmb; ++q)
+          tma_load_2d(dst + 2 * NNT_XBOX_BYTES + q * NNT_MBOX_BYTES, &tmM, k0, q * NNT_MBOX_COLS, fb);
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int wn = warp * 8 * NI;                      // first column of this warp
+  const int pg = (g >> 1) | ((g & 1) << 2);          // fragment column g -> column pg of each 8-block
+  const bool none = wn >= b2;
+  double acc[4][NI][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int c = 0; c < nck; ++c) {
+    const int st = c % ST;
+    mbar_wait(full0 + 8 * st, (c / ST) & 1);
+    const bool idle = none || (tri_upper && c * NNT_KC > wn + 8 * NI - 1);   // M upper: rows k > last column are 0
+    if (!idle) {
+      const unsigned char* xs = base + st * SB;
+      const unsigned char* ms = xs + 2 * NNT_XBOX_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < NNT_KC; kk += 8) {
+        const int k0 = kk + 2 * t, k1 = k0 + 1;      // this lane's k of the two DMMA passes
+        double a0[4], a1[4];
+        double2 b[NI];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int r = 8 * (mi & 1) + g;            // row within the 16-row box mi >> 1
+          const unsigned char* xb = xs + (mi >> 1) * NNT_XBOX_BYTES + ((r & 1) << 3);
+          a0[mi] = *reinterpret_cast<const double*>(xb + k0 * 128 + (((r >> 1) ^ (k0 & 7)) << 4));
+          a1[mi] = *reinterpret_cast<const double*>(xb + k1 * 128 + (((r >> 1) ^ (k1 & 7)) << 4));
+        }
+        const int u = (kk >> 1) + t;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const int col = wn + 8 * ni + pg;          // < 8 * NI * NNT_CONS: inside the staged boxes
+          const unsigned char* mb = ms + (col >> 7) * NNT_MBOX_BYTES + (col & 127) * 128;
+          b[ni] = *reinterpret_cast<const double2*>(mb + ((u ^ (col & 7)) << 4));
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a0[mi], b[ni].x);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a1[mi], b[ni].y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+  }
+  if (none) return;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t r = r0 + 8 * mi + g;
+        const int fc = 2 * t + e;                    // fragment column -> column of the 8-block
+        const int j = wn + 8 * ni + ((fc >> 1) | ((fc & 1) << 2));
+        if (r < n && j < b2) {
+          double* o = Out + r + (int64_t)j * ldo;
+          double v = alpha * acc[mi][ni][e];
+          if (beta != 0.0) v = fma(beta, *o, v);
+          *o = v;
+        }
+      }
+}
+static size_t nnt_smem(int NI) { return (size_t)nnt_stages(NI) * nnt_stage_bytes(NI) + 16 * nnt_stages(NI) + 1024; }
+
 // A (b x b, ld) <- upper triangle mirrored into the strict lower triangle
 __global__ void k_symm_upper(double* __restrict__ A, int b, int64_t ld) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
@@ -724,6 +864,15 @@ static int nn3_min_k() {
   }
   return v;
 }
+// k_gemm_nn_tma for inner dimensions above this (SCSF_NNT_MIN_K)
+static int nnt_min_k() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_NNT_MIN_K");
+    v = e ? atoi(e) : 128;
+  }
+  return v;
+}
 static int nn3_big() {                             // SCSF_NN3_BIG=0: the v1 kernel for b1 > 256
   static int v = -1;
   if (v < 0) {
@@ -749,6 +898,11 @@ int dense_init_attrs() {
                                        (int)nn3_smem(NN2_MAX_K, 64)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn3_smem(NN_MAX_K, 32)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nnt_smem(2)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nnt_smem(3)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nnt_smem(4)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn_tma<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nnt_smem(5)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nnt_smem(6)));
   g_nn_smem_set = 1;
   return SCSF_OK;
 }
@@ -856,7 +1010,21 @@ int gemm_nn_ex(const double* X, int64_t ldx, int64_t n, int b1, const double* M,
   SCSF_TRY(dense_init_attrs());
   const int a16n = ((ldx & 1) == 0 && ((uintptr_t)X & 15) == 0) ? 1 : 0;
   const int m16n = ((ldm & 1) == 0 && ((uintptr_t)M & 15) == 0) ? 1 : 0;
-  if (b1 <= NN2_MAX_K && b1 > nn3_min_k() && b2 > V2_T) {
+  if (b1 > nnt_min_k() && b2 > V2_T && b2 <= NNT_CONS * 8 * 6 && nn_tma_enabled() && tma_layout_ok(X, ldx, n) &&
+      tma_layout_ok(M, ldm, b1)) {
+    SCSF_TRY(tma_encode_fn());
+    CUtensorMap tx, tm;
+    SCSF_TRY(make_tmap(&tx, X, ldx, n, b1, 16, NNT_KC));
+    SCSF_TRY(make_tmap(&tm, M, ldm, b1, b2, NNT_KC, NNT_MBOX_COLS));
+    const int grid = (int)ceil_div(n, NNT_BM);
+    switch ((b2 + NNT_CONS * 8 - 1) / (NNT_CONS * 8)) {     // NI: 8 NI columns per consumer warp
+      case 2: k_gemm_nn_tma<2><<<grid, NNT_NT, nnt_smem(2), s>>>(tx, tm, n, b1, b2, alpha, beta, Out, ldo, tri); break;
+      case 3: k_gemm_nn_tma<3><<<grid, NNT_NT, nnt_smem(3), s>>>(tx, tm, n, b1, b2, alpha, beta, Out, ldo, tri); break;
+      case 4: k_gemm_nn_tma<4><<<grid, NNT_NT, nnt_smem(4), s>>>(tx, tm, n, b1, b2, alpha, beta, Out, ldo, tri); break;
+      case 5: k_gemm_nn_tma<5><<<grid, NNT_NT, nnt_smem(5), s>>>(tx, tm, n, b1, b2, alpha, beta, Out, ldo, tri); break;
+      default: k_gemm_nn_tma<6><<<grid, NNT_NT, nnt_smem(6), s>>>(tx, tm, n, b1, b2, alpha, beta, Out, ldo, tri); break;
+    }
+  } else if (b1 <= NN2_MAX_K && b1 > nn3_min_k() && b2 > V2_T) {
     k_gemm_nn3<64><<<ceil_div(n, 64), 256, nn3_smem(b1, 64), s>>>(X, ldx, n, b1, M, ldm, b2, alpha, beta, Out, ldo,
                                                                  tri, a16n, m16n);
   } else if (b1 > NN2_MAX_K && nn3_big()) {

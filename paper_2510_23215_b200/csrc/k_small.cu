@@ -611,12 +611,32 @@ __global__ void __launch_bounds__(JZ_T) k_jacobi_z(const double2* __restrict__ r
   }
 }
 
+// Conditioning guard of the filter degree.  After the filter the active block's columns differ in
+// size by up to C_m(t_lambda) = cosh(m acosh|t_lambda|) (the scale point against the top of the
+// damped interval) and CholQR's Gram matrix by its square.  On C3 (t_lambda ~ 1.005, acosh ~ 0.10)
+// m <= 192 (C_m <= ~4e8) converged every operator of the full queue while m = 224 / 256 (C_m ~ 1e10
+// / 1e11) left 53 / 130 of 400 unconverged after the shifted-CholQR fallback (R27,
+// profiles/r02_degree_limit_C3.jsonl).  The degree of the next filter is therefore capped so that
+// C_m(t_lambda) <= 1e8 (the Gram matrix then stays at condition <= 1e16 ~ 1 / eps), rounded down to
+// = m (mod 3) (the streaming filter's buffer rotation) and at least 4.  Below the cap m is unchanged.
+__device__ __forceinline__ int filter_degree_cap(double lam, double c, double e, int mdeg) {
+  const double t = fabs((lam - c) / e);
+  if (!(t > 1.0)) return mdeg;
+  const double ach = log(t + sqrt((t - 1.0) * (t + 1.0)));
+  const double lim = 19.113827924512311 / ach;               // acosh(1e8)
+  if (lim >= (double)mdeg) return mdeg;
+  int me = max(4, (int)lim);
+  me = mdeg - 3 * ((mdeg - me + 2) / 3);                      // round down to = mdeg (mod 3)
+  while (me < 4) me += 3;
+  return min(me, mdeg);
+}
+
 // ----------------------------------------------------------------- lock ----
 // theta/res/wn/rel are indexed by block column (0..b-1); active columns [kL, b).
 constexpr double LOCK_FLOOR = 2.0;
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
                        const double* __restrict__ wn, double* __restrict__ rel, int b, int L,
-                       double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg) {
+                       double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg, int cap_on) {
   const int lane = threadIdx.x;            // one warp
   const int kL = ctrl->kL;
   // Reading R26: the test ||r|| <= tol ||Av|| is capped at the fp64 floor of a computed
@@ -657,6 +677,12 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
       fp[0] = lam;
       fp[1] = c;
       fp[2] = e;
+      // cap_on = 0 after the Rayleigh-Ritz step of a random start: its Ritz values say nothing about
+      // the conditioning of the first filtered block (the block's content spans the whole spectrum
+      // far below alpha, so every column is amplified alike)
+      const int me = cap_on ? filter_degree_cap(lam, c, e, mdeg) : mdeg;
+      fp[3] = (double)me;                   // degree of the next filter (streaming / resident kernels)
+      ctrl->pad[2] = me;
     }
   }
   // SURVEY f2 (Alg. 1 l. 5's staggered update, ChASE-style): per-column degree for the next
@@ -669,19 +695,20 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
     __syncwarp();
     const int kLn = ctrl->kL;
     const double c = fp[1], e = fp[2];
+    const int mcap = (int)(fp[3] + 0.5);                     // = mdeg mod 3, so the rounding below holds
     int run = 4, sum = 0;
     for (int base = kLn; base < b; base += 32) {
       const int j = base + lane;
-      int mj = mdeg;
+      int mj = mcap;
       if (j < b) {
         const double t = fabs((theta[j] - c) / e), r = rel[j];
         if (t > 1.0 && isfinite(r)) {
           const double g = t + sqrt((t - 1.0) * (t + 1.0));
           const double need = log(fmax(10.0 * r / tol, 1.0)) / log(g);
-          const int nd = (int)fmin((double)mdeg, fmax(4.0, ceil(need)));
+          const int nd = (int)fmin((double)mcap, fmax(4.0, ceil(need)));
           // round up to nd = m (mod 3): the streaming filter rotates three buffers, so a column
           // that stops after nd steps then holds its Y_nd in the same buffer as Y_m
-          mj = mdeg - 3 * ((mdeg - nd) / 3);
+          mj = mcap - 3 * ((mcap - nd) / 3);
         }
       }
       // running maximum across the columns (lane order, then chunk order)
@@ -704,7 +731,7 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
 }
 
 // First-filter bounds of a warm solve from the previous operator's ascending Ritz values
-__global__ void k_bounds_from_theta(const double* __restrict__ theta, int b, Ctrl* ctrl, double* fp) {
+__global__ void k_bounds_from_theta(const double* __restrict__ theta, int b, Ctrl* ctrl, double* fp, int mdeg) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double lam = theta[0], alpha = theta[b - 1], beta = ctrl->beta;
   double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
@@ -714,6 +741,9 @@ __global__ void k_bounds_from_theta(const double* __restrict__ theta, int b, Ctr
   fp[0] = lam;
   fp[1] = c;
   fp[2] = e;
+  const int me = filter_degree_cap(lam, c, e, mdeg);
+  fp[3] = (double)me;
+  ctrl->pad[2] = me;
 }
 
 __global__ void k_ctrl_init(Ctrl* ctrl, const unsigned long long* gersh) {
@@ -1045,8 +1075,8 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 }
 
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
-              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, cudaStream_t s) {
-  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp, deg, mdeg);
+              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, int cap_on, cudaStream_t s) {
+  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp, deg, mdeg, cap_on);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
@@ -1061,8 +1091,8 @@ int fill_int_impl(int* p, int n, int v, cudaStream_t s) {
   return SCSF_OK;
 }
 
-int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s) {
-  k_bounds_from_theta<<<1, 32, 0, s>>>(theta_sorted, b, ctrl, fp);
+int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, int mdeg, cudaStream_t s) {
+  k_bounds_from_theta<<<1, 32, 0, s>>>(theta_sorted, b, ctrl, fp, mdeg);
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }

@@ -87,15 +87,19 @@ __global__ void k_gershgorin(const double* __restrict__ cf, int dim, int nx, int
 // Out = A X.  The per-step scalars a_s, b_s are tabulated once per filter by k_step_table
 // (step_table_impl, launched before the first step), so a step kernel reads two broadcast values
 // instead of every thread re-running the sigma recurrence up to its step (O(m) divisions each).
-__device__ __forceinline__ void step_scalars(const double* fp, int step, double& a, double& b,
+// Returns false for a step at or past the degree cap (fp[3]): the kernel then does nothing (the cap
+// is = m (mod 3), so the filter's last output still lands in the buffer Y_m would).
+__device__ __forceinline__ bool step_scalars(const double* fp, int step, double& a, double& b,
                                              double& c) {
   if (step < 0) {
     a = 1.0; b = 0.0; c = 0.0;
-    return;
+    return true;
   }
+  if (step >= fp_degree_cap(fp, FP_MAX_DEGREE)) return false;
   c = fp[1];
   a = fp[FP_TAB + 2 * step];
   b = fp[FP_TAB + 2 * step + 1];
+  return true;
 }
 
 // Alg. 1's scalars for steps 0..m-1 (one thread; the recurrence is sequential):
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stencil(
   int64_t k = (int64_t)blockIdx.x * ST_THREADS + threadIdx.x;
   if (k >= n) return;
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int64_t sxy = (int64_t)nx * ny;
   const double dg = cf[k] - c;
   const double xp = cf[ldc + k];
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(VB_THREADS) k_stencil_vib(
     return;
   }
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int64_t o1 = 1, o2 = 2, o3 = nx - 1, o4 = nx, o5 = nx + 1, o6 = 2 * (int64_t)nx;
   const double dg = cf[k] - c;
   const double u1 = cf[ldc + k], u2 = cf[2 * ldc + k], u3 = cf[3 * ldc + k], u4 = cf[4 * ldc + k],
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(VT_T) k_stencil_vib_t(const double* __restrict
   double* sv = vs;                                  // [VT_CB][VW]: rows r0-2 .. r0+VT_R+1
 
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int vbase = (r0 - 2) * nx;
   for (int i = tid; i < VW; i += VT_T) {
     const int k = vbase + i;
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(
   const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
   if (k0 >= ldv) return;
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int64_t sxy = (int64_t)nx * ny;
   int j0 = blockIdx.y * CB;
   const int j1 = min(ncols, j0 + CB);
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4g(
   const int64_t k0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
   if (k0 >= ldv) return;
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int64_t sxy = (int64_t)nx * ny;
   int j0 = blockIdx.y * CB;
   const int j1 = min(ncols, j0 + CB);
@@ -629,6 +633,7 @@ __global__ void __launch_bounds__(RES_T, 1) k_filter_res2d(const double* __restr
                                                            int m) {
   extern __shared__ double rbuf[];               // [2][n]
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  m = fp_degree_cap(fp, m);
   const double* x0 = X + (int64_t)j * ldv;
   double* out = Out + (int64_t)j * ldv;
   const double lam = fp[0], c = fp[1], e = fp[2];
@@ -794,6 +799,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+  m = fp_degree_cap(fp, m);                               // conditioning guard (k_lock)
   const int R = ((ny + CS - 1) / CS + 1) & ~1;
   const int row0 = rank * R;
   const int rows = max(0, min(R, ny - row0));
@@ -1024,6 +1030,7 @@ __global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict_
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int j0 = blockIdx.y * CB, tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+  m = fp_degree_cap(fp, m);                               // conditioning guard (k_lock)
   const int R = ((ny + CS - 1) / CS + RP_ROWS - 1) / RP_ROWS * RP_ROWS;
   const int row0 = rank * R;
   const int rows = max(0, min(R, ny - row0));
@@ -1315,7 +1322,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
   const int64_t l0 = l_begin + ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;   // local point
   if (l0 >= l_end) return;
   double a, b, c;
-  step_scalars(fp, step, a, b, c);
+  if (!step_scalars(fp, step, a, b, c)) return;
   const int j0 = blockIdx.y * CB;
   const int j1 = min(ncols, j0 + CB);
   if (l0 >= n_loc) {                                  // ld padding

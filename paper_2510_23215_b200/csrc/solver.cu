@@ -16,6 +16,7 @@
 #include "comm.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -55,9 +56,9 @@ int chol_inv_impl(const double* S, int64_t lds, int b, int64_t nrows, double* Ri
 int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z, double* theta,
                 double* Zout, Ctrl* ctrl, cudaStream_t s);
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
-              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, cudaStream_t s);
+              double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, int cap_on, cudaStream_t s);
 int ctrl_init_impl(Ctrl* ctrl, const unsigned long long* gersh, cudaStream_t s);
-int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, cudaStream_t s);
+int bounds_from_theta_impl(const double* theta_sorted, int b, Ctrl* ctrl, double* fp, int mdeg, cudaStream_t s);
 int step_table_impl(double* fp, int m, cudaStream_t s);
 int rand_block_impl(double* V, int64_t ldv, int64_t n, int ncols, uint64_t seed, int64_t goff, cudaStream_t s);
 int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncols, double* send_lo,
@@ -294,7 +295,7 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
     SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
   }
-  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, s));
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, w.cap_on, s));
   return SCSF_OK;
 }
 
@@ -349,7 +350,7 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
     SCSF_TRY(w.comm->allreduce_sum(w.res + k0, ba, s));
     SCSF_TRY(w.comm->allreduce_sum(w.wn + k0, ba, s));
   }
-  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, s));
+  SCSF_TRY(lock_impl(w.theta, w.res, w.wn, w.rel, w.b, L, tol, w.ctrl, w.fp, w.deg_on, w.mdeg, w.cap_on, s));
   return SCSF_OK;
 }
 
@@ -361,6 +362,16 @@ static bool inherit_bounds() {
   if (v < 0) {
     const char* e = getenv("SCSF_INHERIT_BOUNDS");
     v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// SCSF_TRACE=1: one stderr line per outer iteration (diagnostics for tools/; host reads only)
+static bool trace_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_TRACE");
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
@@ -576,18 +587,24 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
     SCSF_TRY(cholqr_pass(w, w.V, w.V, b, s));
   }
+  w.cap_on = warm ? 1 : 0;
   if (warm && !orthonormalize && inherit_bounds()) {
     // P:193-194, P:297 read literally: the first filter of a warm solve uses the previous
     // operator's Ritz values (lambda = theta_1, alpha = theta_b) and this operator's beta
-    SCSF_TRY(bounds_from_theta_impl(w.theta_sorted, b, w.ctrl, w.fp, s));
+    SCSF_TRY(bounds_from_theta_impl(w.theta_sorted, b, w.ctrl, w.fp, degree, s));
+    SCSF_TRY(read_ctrl(w, h, s));
   } else {
     // one Rayleigh-Ritz of the new operator on the initial block (R11)
     SCSF_TRY(rayleigh_ritz(ops, op, w, 0, L, tol, spmm_cols, s));
     SCSF_TRY(read_ctrl(w, h, s));
   }
+  w.cap_on = 1;
   int kL = h.kL;
   int fallbacks = 0;
-  int64_t next_colsteps = (int64_t)degree * (b - kL);      // per-column degrees start at m
+  // degree the next filter runs: m, or the conditioning cap k_lock / k_bounds_from_theta wrote
+  // (ctrl->pad[2], = fp[3]; the kernels apply it on the device, the host only counts with it)
+  auto filter_degree = [&](const Ctrl& c) { return (c.pad[2] > 0 && c.pad[2] < degree) ? (int)c.pad[2] : degree; };
+  int64_t next_colsteps = (int64_t)filter_degree(h) * (b - kL);   // per-column degrees start at m
   // One outer iteration (steps 1-6) as device work only; replayed from a CUDA graph
   // keyed by kL (every pointer and shape of the iteration is a function of kL).
   auto iteration = [&](int kLc) -> int {
@@ -665,14 +682,19 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
     // algorithmic bytes: first step reads Y0 + writes Y1, later steps read Y_s, Y_{s-1}
     // and write Y_{s+1}; one pass over the coefficient arrays per step
     // column-steps of this filter: m b_act, or the sum of the per-column degrees (f2)
-    const int64_t colsteps = w.deg_on ? next_colsteps : (int64_t)degree * ba;
-    filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * (double)(colsteps - ba) + coef_bytes * degree;
-    filter_steps += degree;
+    const int m_it = filter_degree(h);
+    const int64_t colsteps = w.deg_on ? next_colsteps : (int64_t)m_it * ba;
+    filter_bytes += 16.0 * w.n * ba + 24.0 * w.n * (double)(colsteps - ba) + coef_bytes * m_it;
+    filter_steps += m_it;
     spmm_cols += colsteps + 2 * ba;
     SCSF_TRY(read_ctrl(w, h, s));
     SCSF_TRY(tm.accumulate());
     SCSF_TRY(gt_collect());
     next_colsteps = h.pad[1];
+    if (trace_enabled())
+      fprintf(stderr, "[scsf trace] op %d warm %d it %d m %d kL %d lambda %.6e alpha %.6e beta %.6e next_m %d "
+              "chol_fail %d nonfinite %d max_rel %.3e\n", op_in, warm ? 1 : 0, iters, m_it, h.kL, h.lambda, h.alpha,
+              h.beta, filter_degree(h), h.chol_fail, h.nonfinite, h.max_rel);
     if (h.chol_fail) {
       // shifted CholQR was needed: one more CholQR pass, then redo the RR step
       ++fallbacks;
@@ -725,7 +747,7 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
     }
   }
   if (status != SCSF_OK)
-    set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op,
+    set_error("operator %d: %d of %d pairs converged after %d iterations (worst rel. residual %.3e)", op_in,
               kL, L, iters, h.max_rel);
   return status;
 }

@@ -24,6 +24,7 @@ struct SolveWS {
   int* deg = nullptr;                                                  // per-column filter degree
   int* deg_on = nullptr;                                               // == deg when the adaptive degree is on
   int mdeg = 20;
+  int cap_on = 1;       // k_lock applies the degree cap (R28); 0 for the RR of a random start
   int b = 0;
   double *V = nullptr, *W = nullptr, *T1 = nullptr, *T2 = nullptr;   // n x b blocks (ld ldv)
   double *S = nullptr, *Rinv = nullptr, *Zs = nullptr, *Zwork = nullptr, *Gwork = nullptr;  // b x b

@@ -61,7 +61,7 @@ class scsf_stats(ctypes.Structure):
                 ("spmm_columns", ctypes.c_int64), ("max_rel_resid", ctypes.c_double),
                 ("beta", ctypes.c_double), ("t_filter_ms", ctypes.c_double), ("t_ortho_ms", ctypes.c_double),
                 ("t_rr_ms", ctypes.c_double), ("filter_bytes", ctypes.c_double),
-                ("jacobi_sweeps", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("jacobi_sweeps", ctypes.c_int32), ("cold_retry", ctypes.c_int32),
                 ("t_gemm_ms", ctypes.c_double), ("gemm_flops", ctypes.c_double)]
 
     def as_dict(self):

@@ -68,8 +68,13 @@ def test_gemm_tn_upper(lib, n, b):
 
 @pytest.mark.parametrize("n,b1,b2,beta", [(10000, 120, 120, 0.0), (1001, 7, 130, -1.0), (333, 128, 33, 0.5),
                                           (5000, 240, 240, 0.0), (64, 1, 1, 1.0), (3001, 360, 360, 0.0),
-                                          (777, 300, 70, 1.0), (100, 257, 129, -0.5)])
+                                          (777, 300, 70, 1.0), (100, 257, 129, -0.5), (4099, 130, 250, 1.0),
+                                          (70001, 368, 300, -1.0), (2000, 200, 384, 0.0), (65, 144, 129, 0.5),
+                                          (3000, 200, 100, 0.0), (5000, 129, 180, 2.0)])
 def test_gemm_nn(lib, n, b1, b2, beta):
+    """Every NN kernel: b1 > 128, b2 > 64 with even leading dimensions take the TMA-fed whole-row
+    kernel (k_gemm_nn_tma<NI>, NI = ceil(b2 / 64) = 2..6; ragged n, b1, b2 zero-filled by the
+    tensor maps); odd ldm, b1 <= 128 or b2 <= 64 the cp.async kernels."""
     import torch
     rng = np.random.default_rng(n + b2)
     X = rng.standard_normal((n, b1))

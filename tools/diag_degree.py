@@ -22,4 +22,7 @@ bad = [(k, s) for k, s in enumerate(st) if s["status"] != 0]
 print(json.dumps({"m": m, "N": N, "failed": len(bad),
                   "examples": [{"pos": k, "status": s["status"], "iterations": s["iterations"], "n_locked": s["n_locked"],
                                 "max_rel_resid": s["max_rel_resid"], "fallbacks": s["cholqr_fallbacks"],
-                                "warm": s["warm"]} for k, s in bad[:8]]}))
+                                "warm": s["warm"], "op": int(perm[k]), "filter_steps": s["filter_steps"]}
+                               for k, s in bad[:8]],
+                  "filter_steps": int(sum(s["filter_steps"] for s in st)),
+                  "iterations": int(sum(s["iterations"] for s in st))}))
