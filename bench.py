@@ -290,6 +290,22 @@ def roofline_objects(scsf, cfg, ops, rst, r_ms, degree, step_ms_per_op, hbm, hbm
                "launches": launches_f, "avg_launch_us": 1000.0 * fms / max(launches_f, 1),
                "bytes_per_launch": fbytes / max(launches_f, 1),
                "share_of_single_chain_time": fms / r_ms if r_ms > 0 else None}
+    if kind > 0 and fms > 0:
+        # the on-chip bound of the resident kernel: the fp64 FMA pipe.  Algorithmic flops per point, column
+        # and step of Alg. 1 l. 5: (A - cI) y (2 (2d + 1) - 1 flops) and the recurrence a (.) + b Y_{s-1}
+        # (3 flops): 12 in 2-D, 16 in 3-D; columns per launch from the streaming-form byte count above
+        m_ = abs(degree)
+        per = fbytes / max(launches_f, 1) - 8.0 * (1 + cfg.dim) * cfg.n * m_
+        cols = per / ((16.0 + 24.0 * (m_ - 1)) * cfg.n)
+        fl = cols * cfg.n * m_ * (4.0 * cfg.dim + 4.0) * launches_f
+        dfma, dfma_src = fp64_alu_peak()
+        a_tf = fl / (fms / 1000.0) / 1e12
+        hbm_obj["roofline_alu"] = {
+            "bound": "alu", "kernel": kname, "achieved": a_tf, "peak": dfma, "unit": "TFLOP/s",
+            "frac": a_tf / dfma, "peak_source": dfma_src,
+            "achieved_is": f"algorithmic fp64 flops of the recurrence ({int(4 * cfg.dim + 4)} per point, column and "
+                           "step) / filter time: the kernel's on-chip ceiling (its steps never touch DRAM)",
+            "flops_per_launch": fl / max(launches_f, 1)}
     dmma_obj = None
     if gms > 0:
         a = gfl / (gms / 1000.0) / 1e12
@@ -302,6 +318,17 @@ def roofline_objects(scsf, cfg, ops, rst, r_ms, degree, step_ms_per_op, hbm, hbm
                     "share_of_single_chain_time": gms / r_ms if r_ms > 0 else None}
     phases = {"filter": fms, "ortho": oms, "rayleigh_ritz": rms, "gemm": gms, "total": r_ms}
     return hbm_obj, dmma_obj, phases
+
+
+def fp64_alu_peak():
+    """Measured DFMA throughput of this B200 (tools/fp64_pipes.cu -> profiles/r02_fp64_pipes.json), else the
+    nominal 148 SMs x 64 DFMA/clk x 2 flops x 1.965 GHz."""
+    p = os.path.join(ROOT, "profiles", "r02_fp64_pipes.json")
+    try:
+        j = json.load(open(p))
+        return float(j["dfma_tflops"]), "profiles/r02_fp64_pipes.json: DFMA, tools/fp64_pipes.cu on a B200 of this pool"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal: 148 SMs x 64 DFMA/clk x 2 flops x 1.965 GHz"
 
 
 def stream_probe(scsf, torch, cfg, ops, degree, hbm):
@@ -565,7 +592,8 @@ def run_chains(args, cfg, degree, rank, world, local, dev, torch, dist, scsf, hb
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded GRF coefficient fields, DESIGN.md §3)",
-                "config": conf, "roofline": hbm_obj, "roofline_dmma": dmma_obj, "roofline_streaming": streaming,
+                "config": conf, "roofline": hbm_obj, "roofline_alu": hbm_obj.pop("roofline_alu", None),
+                "roofline_dmma": dmma_obj, "roofline_streaming": streaming,
                 "single_chain_phase_ms": phases, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(round(launches)), "clocks": clk,
                 "converged": f"{conv}/{len(all_stats)}", "iterations_mean": float(np.mean(iters)) if iters else None,
@@ -677,7 +705,8 @@ def run_rowpart(args, cfg, degree, rank, world, local, dev, torch, dist, scsf, h
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded GRF coefficient fields, DESIGN.md §3)",
-                "config": conf, "roofline": hbm_obj, "roofline_dmma": dmma_obj, "single_chain_phase_ms": phases,
+                "config": conf, "roofline": hbm_obj, "roofline_alu": hbm_obj.pop("roofline_alu", None),
+                "roofline_dmma": dmma_obj, "single_chain_phase_ms": phases,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches)), "clocks": clk,
                 "converged": f"{conv}/{len(all_stats)}", "iterations_mean": float(np.mean(iters)) if iters else None,
                 "iterations_max": int(max(iters)) if iters else None}

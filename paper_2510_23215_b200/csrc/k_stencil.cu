@@ -15,6 +15,7 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <type_traits>
 #include <mutex>
 
 #include <cooperative_groups.h>
@@ -723,12 +724,15 @@ __device__ __forceinline__ void sts4(double* p, double4 v) {
 // HBM traffic per filter and column: read Y_0, write Y_m (16 n B) plus the
 // coefficient arrays once per CB columns.  Bound: shared-memory bandwidth
 // (~32 B per point per step) and the cluster barrier (amortised over CB).
-constexpr int CL_T = 768;                        // max threads per CTA (<= 85 registers each)
+constexpr int CL_T = 768;                        // max threads per CTA (<= 80 registers: 6 warps per SMSP quadrant)
 constexpr int CL_MAXP = CL_T;                    // 2 x 2 patches per CTA
 
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// the two halves (every thread of the cluster alternates arrive / wait; warp-uniform call sites)
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
@@ -783,6 +787,11 @@ __device__ __forceinline__ unsigned mapa32(unsigned a, unsigned rank) {
 __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// the same store at a + d, the add inside the asm: the compiler cannot hoist (and spill) a + d per column
+__device__ __forceinline__ void stc2ad(unsigned a, unsigned d, double2 v) {
+  asm volatile("{\n\t.reg .u32 t;\n\tadd.u32 t, %0, %1;\n\tst.shared::cluster.v2.f64 [t], {%2, %3};\n\t}"
+               ::"r"(a), "r"(d), "d"(v.x), "d"(v.y) : "memory");
+}
 
 // TM: the thread's own patch rows of Y_s and Y_{s-1} live in tensor memory (two 8-word slots per
 // column, roles swapped every step) instead of being re-read from the shared buffers: per step and
@@ -792,7 +801,7 @@ template <int CS, int CB, bool TM = false>
 __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
-                                                       const int* __restrict__ deg) {
+                                                       const int* __restrict__ deg, int split) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
   __shared__ double sa[FP_MAX_DEGREE], sb[FP_MAX_DEGREE]; // per-step scalars (m <= FP_MAX_DEGREE)
@@ -894,7 +903,9 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   // and my row(s) in the CTA above's bottom ghost row, as deltas to my own target address
   const unsigned lo32 = has_lo ? mapa32(sbase, rank - 1) : 0u, hi32 = has_hi ? mapa32(sbase, rank + 1) : 0u;
   const unsigned dlo = lo32 - sbase + (unsigned)R * nx8;                 // local row 0 -> row R + 1 below
-  const unsigned dhi = hi32 - sbase - (unsigned)(lr0 + 1) * nx8;         // local row r  -> row 0 above
+  // local row rows - 1 -> row 0 above; the same (CTA-uniform) delta serves a lower row (push_hi0,
+  // lr0 = rows - 1) and an upper row (push_hi1, at na + nx8)
+  const unsigned dhi = hi32 - sbase - (unsigned)rows * nx8;
   cluster_barrier();                                       // also publishes sa / sb
   __shared__ unsigned tm_base_s;
   unsigned tbase = 0;                                      // this thread's TMEM address (lane, column 0)
@@ -921,73 +932,106 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     }
     tmem_wait_st();
   }
-  for (int st = 0; st < mrun; ++st) {
+  // One step of Alg. 1 for the CB columns.  PAR = st & 1 is a compile-time constant (the loop
+  // below runs two steps per trip), so the buffer roles and the TMEM slot roles are static: a
+  // stepped column's buffers swap every step, hence at step st its current buffer is 2 cc + PAR
+  // (a column past its own degree is not stepped again; its final buffer is mcol & 1).  With the
+  // parity in a register the compiler spent 16 FSEL per column and step on the slot swap.
+  const bool push_any = push_lo0 || push_hi0 || push_hi1;
+  const unsigned abuf0 = sbase + 8u * (unsigned)l0, pitch8 = 8u * (unsigned)pitch;
+  auto step = [&](auto par, int st) {
+    constexpr int PAR = decltype(par)::value;
     const double a = sa[st], bco = sb[st];
-    {
 #pragma unroll
-      for (int cc = 0; cc < CB; ++cc) {
-        if (st < mcol[cc]) {                               // uniform across the CTA (0 beyond ncb)
-          const unsigned ca = acur[cc], na = anxt[cc];
-          const double2 xd = lds2a(ca - nx8);
-          double2 xa, xb, p0, p1;
-          const unsigned tcur = tbase + cc * 16 + 8 * (st & 1), tprev = tbase + cc * 16 + 8 * ((st + 1) & 1);
-          if (TM) {
-            double2 q0, q1;
-            tmem_ld16(tbase + cc * 16, q0, q1, p0, p1);          // both slots: Y_s and Y_{s-1}
-            if (st & 1) {
-              xa = p0; xb = p1; p0 = q0; p1 = q1;
-            } else {
-              xa = q0; xb = q1;
-            }
-            if (!up_ok) xb = lds2a(ca + nx8);                    // no upper row: the ghost row above
+    for (int cc = 0; cc < CB; ++cc) {
+      if (st < mcol[cc]) {                                 // uniform across the CTA (0 beyond ncb)
+        // buffer b of column cc starts b * pitch doubles after buffer 0: 2 cc + PAR is current
+        const unsigned ca = abuf0 + (unsigned)(2 * cc + PAR) * pitch8, na = abuf0 + (unsigned)(2 * cc + 1 - PAR) * pitch8;
+        const double2 xd = lds2a(ca - nx8);
+        double2 xa, xb, p0, p1;
+        if (TM) {
+          double2 q0, q1;
+          tmem_ld16(tbase + cc * 16, q0, q1, p0, p1);      // both slots: Y_s and Y_{s-1}
+          if (PAR) {
+            xa = p0; xb = p1; p0 = q0; p1 = q1;
           } else {
-            xa = lds2a(ca);
-            xb = lds2a(ca + nx8);
+            xa = q0; xb = q1;
           }
-          const double2 xu = lds2a(ca + up8);
-          double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
-          double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
-          if (fix_l) {
-            xal = lds1a(ca - 8u);
-            xbl = lds1a(ca + nx8 - 8u);
-          }
-          if (fix_r) {
-            xar = lds1a(ca + 16u);
-            xbr = lds1a(ca + nx8 + 16u);
-          }
-          double2 v, u;
-          v.x = fma(dg0.x, xa.x, fma(cxp0.x, xa.y, fma(cxm0, xal, fma(cyp0.x, xb.x, cym0.x * xd.x))));
-          v.y = fma(dg0.y, xa.y, fma(cxp0.y, xar, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
-          u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
-          u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
-          // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
-          if (!TM) {
-            p0 = lds2a(na);
-            p1 = lds2a(na + nx8);
-          }
-          v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
-          u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
-          if (act) sts2a(na, v);
-          if (up_ok) sts2a(na + nx8, u);
-          // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas)
-          if (push_lo0) stc2a(na + dlo, v);
-          if (push_hi0) stc2a(na + dhi, v);
-          if (push_hi1) stc2a(na + dhi, u);
-          if (TM) tmem_st8(tprev, v, u);                         // Y_{s+1} replaces Y_{s-1}
-          (void)tcur;
+          if (!up_ok) xb = lds2a(ca + nx8);                // no upper row: the ghost row above
+        } else {
+          xa = lds2a(ca);
+          xb = lds2a(ca + nx8);
         }
+        const double2 xu = lds2a(ca + up8);
+        double xal = __shfl_up_sync(0xffffffffu, xa.y, 1), xar = __shfl_down_sync(0xffffffffu, xa.x, 1);
+        double xbl = __shfl_up_sync(0xffffffffu, xb.y, 1), xbr = __shfl_down_sync(0xffffffffu, xb.x, 1);
+        if (fix_l) {
+          xal = lds1a(ca - 8u);
+          xbl = lds1a(ca + nx8 - 8u);
+        }
+        if (fix_r) {
+          xar = lds1a(ca + 16u);
+          xbr = lds1a(ca + nx8 + 16u);
+        }
+        double2 v, u;
+        v.x = fma(dg0.x, xa.x, fma(cxp0.x, xa.y, fma(cxm0, xal, fma(cyp0.x, xb.x, cym0.x * xd.x))));
+        v.y = fma(dg0.y, xa.y, fma(cxp0.y, xar, fma(cxp0.x, xa.x, fma(cyp0.y, xb.y, cym0.y * xd.y))));
+        u.x = fma(dg1.x, xb.x, fma(cxp1.x, xb.y, fma(cxm1, xbl, fma(cyp1.x, xu.x, cyp0.x * xa.x))));
+        u.y = fma(dg1.y, xb.y, fma(cxp1.y, xbr, fma(cxp1.x, xb.x, fma(cyp1.y, xu.y, cyp0.y * xa.y))));
+        // Y_{s-1} sits in the target buffer (zero at s = 0: bco = 0 there, and the buffer holds finite values)
+        if (!TM) {
+          p0 = lds2a(na);
+          p1 = lds2a(na + nx8);
+        }
+        v.x = fma(bco, p0.x, a * v.x); v.y = fma(bco, p0.y, a * v.y);
+        u.x = fma(bco, p1.x, a * u.x); u.y = fma(bco, p1.y, a * u.y);
+        if (act) sts2a(na, v);
+        if (up_ok) sts2a(na + nx8, u);
+        // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas);
+        // a branch, not predication: only the warps holding a slab's first / last row take it
+        if (push_any) {
+          if (push_lo0) stc2ad(na, dlo, v);
+          if (push_hi0) stc2ad(na, dhi, v);
+          if (push_hi1) stc2ad(na, nx8 + dhi, u);
+        }
+        if (TM) tmem_st8(tbase + cc * 16 + 8 * (1 - PAR), v, u);   // Y_{s+1} replaces Y_{s-1}
       }
-      if (TM) tmem_wait_st();
     }
-#pragma unroll
-    for (int cc = 0; cc < CB; ++cc)                        // the buffers swap roles for every column stepped
-      if (st < mcol[cc]) {
-        const unsigned t = acur[cc];
-        acur[cc] = anxt[cc];
-        anxt[cc] = t;
-      }
-    cluster_barrier();                                     // nxt (and pushed ghosts) complete cluster-wide
+    if (TM) tmem_wait_st();
+  };
+  // Step synchronisation.  Default: one cluster barrier per step (nxt and the pushed ghost rows complete
+  // cluster-wide).  split != 0: the barrier is split into arrive / wait, and only the warps that read a
+  // ghost row (a patch in the slab's first or last patch row; warp-uniform, so shuffles and the .aligned
+  // barriers stay converged) wait for the cluster before computing a step; the interior warps compute the
+  // step right after the CTA barrier and wait afterwards, so the cluster-barrier latency overlaps their
+  // work.  Ordering: the interior rows a warp reads come from its own CTA (__syncthreads of the previous
+  // step); ghost rows are pushed by the neighbours' edge warps before their arrive (release) and read
+  // after my wait (acquire); a push of step s + 1 into buffer ca(s) happens after the pusher's wait of
+  // step s, i.e. after every thread of this CTA finished reading ca(s) in step s.
+  const bool edge_w = __any_sync(0xffffffffu, (lr0 == 0) || (lr0 + 2 >= rows));
+  auto pre = [&](int st) {
+    if (split && st > 0 && edge_w) cluster_wait();
+  };
+  auto post = [&](int st) {
+    if (split) {
+      if (st > 0 && !edge_w) cluster_wait();
+      cluster_arrive();
+      __syncthreads();
+    } else {
+      cluster_barrier();
+    }
+  };
+  for (int st = 0; st < mrun; st += 2) {
+    pre(st);
+    step(std::integral_constant<int, 0>{}, st);
+    post(st);
+    if (st + 1 < mrun) {
+      pre(st + 1);
+      step(std::integral_constant<int, 1>{}, st + 1);
+      post(st + 1);
+    }
   }
+  if (split && mrun > 0) cluster_wait();                   // the last arrive: no CTA leaves while pushed to
   if (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -1023,7 +1067,7 @@ template <int CS, int CB>
 __global__ void __launch_bounds__(RP_T, 1) k_filter_rp(const double* __restrict__ cf, int64_t ldc, int nx, int ny,
                                                        const double* __restrict__ X, int64_t ldv, int ncols,
                                                        double* __restrict__ Out, const double* __restrict__ fp, int m,
-                                                       const int* __restrict__ deg) {
+                                                       const int* __restrict__ deg, int /*split: k_filter_cl only*/) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double cbuf[];           // [CB][2][R + 2][nx]
   __shared__ double sa[FP_MAX_DEGREE], sb[FP_MAX_DEGREE];
@@ -1506,8 +1550,8 @@ int stencil_init_attrs();
 template <int CS, int CB, bool TM>
 __global__ void k_filter_cl(const double* __restrict__ cf, int64_t ldc, int nx, int ny, const double* __restrict__ X,
                             int64_t ldv, int ncols, double* __restrict__ Out, const double* __restrict__ fp, int m,
-                            const int* __restrict__ deg);
-// Can this device co-schedule a 16-CTA cluster of the largest filter CTA (768 threads, 200 KB)?
+                            const int* __restrict__ deg, int split);
+// Can this device co-schedule a 16-CTA cluster of the largest filter CTA (CL_T threads, 200 KB)?
 // Probed once inside stencil_init_attrs() (std::call_once, before any chain thread launches);
 // a device that cannot (fewer SMs per GPC, partitioned GPUs) keeps clusters <= 8.
 static std::atomic<int> g_cs16{-1};
@@ -1595,12 +1639,21 @@ static bool filter_tmem(unsigned threads) {
   const char* e = getenv("SCSF_FILTER_TMEM");
   return !(e && e[0] == '0');
 }
+// The split arrive / wait step synchronisation of k_filter_cl is the default; SCSF_FILTER_SPLIT = 0
+// restores one cluster barrier per step (read per call).  Measured (tools/bench_filter.py, m = 160,
+// profiles/r02_filter_split_ab.json): C3 filter 3.611 -> 3.489 ms, C2 0.440 -> 0.431 ms; C3 bench
+// 45.5 -> 46.5 operators/s.
+static int filter_split() {
+  const char* e = getenv("SCSF_FILTER_SPLIT");
+  return (e && e[0] == '0') ? 0 : 1;
+}
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
+  const int split = filter_split();
   if (filter_tmem(cfg.blockDim.x))
-    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, false>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, true>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, split);
+  return cudaLaunchKernelEx(&cfg, k_filter_cl<CS, CB, false>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, split);
 }
 template <int CS>
 static cudaError_t launch_cl_cb(cudaLaunchConfig_t& cfg, int cb, const double* cf, int64_t ldc, int nx, int ny,
@@ -1614,10 +1667,10 @@ static cudaError_t launch_rp(cudaLaunchConfig_t& cfg, int cs, const double* cf, 
                              const double* X, int64_t ldv, int ncols, double* Out, const double* fp, int m,
                              const int* deg) {
   switch (cs) {
-    case 1: return cudaLaunchKernelEx(&cfg, k_filter_rp<1, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-    case 2: return cudaLaunchKernelEx(&cfg, k_filter_rp<2, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-    case 4: return cudaLaunchKernelEx(&cfg, k_filter_rp<4, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
-    default: return cudaLaunchKernelEx(&cfg, k_filter_rp<8, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg);
+    case 1: return cudaLaunchKernelEx(&cfg, k_filter_rp<1, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, 0);
+    case 2: return cudaLaunchKernelEx(&cfg, k_filter_rp<2, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, 0);
+    case 4: return cudaLaunchKernelEx(&cfg, k_filter_rp<4, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, 0);
+    default: return cudaLaunchKernelEx(&cfg, k_filter_rp<8, RP_CB>, cf, ldc, nx, ny, X, ldv, ncols, Out, fp, m, deg, 0);
   }
 }
 static cudaError_t launch_cl(cudaLaunchConfig_t& cfg, int cs, int cb, const double* cf, int64_t ldc, int nx, int ny,

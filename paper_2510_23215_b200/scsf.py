@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libscsf.so")
+# SCSF_LIB: another in-tree build of the same library (A/B measurements of a kernel variant)
+LIB_PATH = os.environ.get("SCSF_LIB") or os.path.join(_HERE, "lib", "libscsf.so")
 
 SCSF_OK, SCSF_ERR_ARG, SCSF_ERR_NUMERICAL, SCSF_ERR_DEVICE, SCSF_ERR_NOT_IMPLEMENTED, SCSF_ERR_WORKSPACE = range(6)
 _STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NUMERICAL", 3: "ERR_DEVICE", 4: "ERR_NOT_IMPLEMENTED", 5: "ERR_WORKSPACE"}

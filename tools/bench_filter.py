@@ -1,5 +1,6 @@
 """Filter (Alg. 1) microbenchmark: scsf_cheb_filter on full-width blocks at the config shapes."""
 import json
+import os
 import sys
 
 import numpy as np
@@ -19,7 +20,7 @@ def main():
         ops = scsf.assemble(cfg.dim, cfg.nx, cfg.h, faces, torch.from_numpy(f.c).cuda())
         n, ld, b = cfg.n, ops.ld, cfg.b
         Y0 = torch.randn(b, ld, dtype=torch.float64, device="cuda")
-        m = cfg.degree
+        m = int(os.environ.get("BF_DEGREE", cfg.degree))
         for _ in range(2):
             scsf.cheb_filter(ops, 0, Y0, m, 30.0, 5e4, 4e4)
         torch.cuda.synchronize()
