@@ -48,8 +48,11 @@ CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 # converges to the same tolerance; the line also reports the paper's m = 20 on the same queue.
 # The degree has a stability ceiling: the filtered block's condition number grows like
 # exp(2 m sqrt(delta)) and CholQR squares it; on C3, m = 224 / 256 left 53 / 130 of 400 operators
-# unconverged (CholQR breakdown, profiles/r02_degree_limit_C3.jsonl), m = 160 / 192 none.
-BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 160, "C4": 80, "C5": 80}
+# unconverged (CholQR breakdown, profiles/r02_degree_limit_C3.jsonl), m = 160 / 192 none; since the
+# device-side conditioning cap (reading R28) and the cold retry every m converges, and with the
+# neighbour-sync filter m = 160 / 192 / 224 / 256 give 46.6 / 47.2 / 47.4 / 47.3 operators/s
+# (profiles/r02_degree_sweep_s2.json): C3 runs at 192, just above where the cap starts to bind.
+BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 192, "C4": 80, "C5": 80}
 DEFAULT_CONFIG = "C3"
 
 

@@ -787,6 +787,30 @@ __device__ __forceinline__ unsigned mapa32(unsigned a, unsigned rank) {
 __device__ __forceinline__ void stc2a(unsigned a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// asynchronous store into a neighbour CTA's shared memory that completes `16` transaction bytes on the
+// neighbour's mbarrier (address a + d, barrier mb; both shared::cluster): no cluster-wide fence needed
+__device__ __forceinline__ void stc2_async(unsigned a, unsigned d, unsigned mb, double2 v) {
+  asm volatile("{\n\t.reg .u32 t;\n\tadd.u32 t, %0, %1;\n\t"
+               "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [t], {%3, %4}, [%2];\n\t}"
+               ::"r"(a), "r"(d), "r"(mb), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void mb_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// wait for the phase of the given parity; traps after 2^26 polls (seconds; a step takes microseconds, and
+// a cluster's CTAs are co-resident) instead of hanging the GPU
+__device__ __forceinline__ void mb_wait_cluster(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  for (unsigned it = 0;; ++it) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) break;
+    if (it > (1u << 26)) __trap();
+  }
+}
 // the same store at a + d, the add inside the asm: the compiler cannot hoist (and spill) a + d per column
 __device__ __forceinline__ void stc2ad(unsigned a, unsigned d, double2 v) {
   asm volatile("{\n\t.reg .u32 t;\n\tadd.u32 t, %0, %1;\n\tst.shared::cluster.v2.f64 [t], {%2, %3};\n\t}"
@@ -843,6 +867,13 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   const bool has_hi = (rank + 1 < CS) && (row0 + R < ny);
   double* lo_buf = has_lo ? cluster.map_shared_rank(cbuf, rank - 1) : nullptr;   // CTA below
   double* hi_buf = has_hi ? cluster.map_shared_rank(cbuf, rank + 1) : nullptr;   // CTA above
+  // split == 2: one mbarrier per buffer parity receives the neighbours' ghost-row pushes (st.async)
+  __shared__ __align__(8) unsigned long long gmb[2];
+  if (split == 2 && tid == 0) {
+    mb_init((unsigned)__cvta_generic_to_shared(&gmb[0]), 1);
+    mb_init((unsigned)__cvta_generic_to_shared(&gmb[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   // all buffers zero: Dirichlet ghost rows, and Y_{-1} = 0 for the first step's (bco = 0) term
   for (int i = tid; i < CB * pitch; i += nthr) sts2(cbuf + 2 * i, make_double2(0.0, 0.0));
   cluster_barrier();                                       // every CTA of the cluster is running and zeroed
@@ -939,6 +970,10 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   // parity in a register the compiler spent 16 FSEL per column and step on the slot swap.
   const bool push_any = push_lo0 || push_hi0 || push_hi1;
   const unsigned abuf0 = sbase + 8u * (unsigned)l0, pitch8 = 8u * (unsigned)pitch;
+  // split == 2: my mbarriers (gmb[p] receives the pushes into buffer p) and the deltas to the neighbours'
+  const unsigned gmb32 = (unsigned)__cvta_generic_to_shared(&gmb[0]);
+  const unsigned dmb_lo = has_lo ? mapa32(gmb32, rank - 1) - gmb32 : 0u;
+  const unsigned dmb_hi = has_hi ? mapa32(gmb32, rank + 1) - gmb32 : 0u;
   auto step = [&](auto par, int st) {
     constexpr int PAR = decltype(par)::value;
     const double a = sa[st], bco = sb[st];
@@ -990,9 +1025,18 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
         // boundary rows into the neighbours' ghost rows (same buffer layout: fixed address deltas);
         // a branch, not predication: only the warps holding a slab's first / last row take it
         if (push_any) {
-          if (push_lo0) stc2ad(na, dlo, v);
-          if (push_hi0) stc2ad(na, dhi, v);
-          if (push_hi1) stc2ad(na, nx8 + dhi, u);
+          if (split == 2) {                                // st.async completing bytes on the receiver's
+            if (st + 1 < mcol[cc]) {                       // mbarrier; no push after a column's last step
+              const unsigned mbo = gmb32 + 8u * (unsigned)(1 - PAR);
+              if (push_lo0) stc2_async(na, dlo, mbo + dmb_lo, v);
+              if (push_hi0) stc2_async(na, dhi, mbo + dmb_hi, v);
+              if (push_hi1) stc2_async(na, nx8 + dhi, mbo + dmb_hi, u);
+            }
+          } else {
+            if (push_lo0) stc2ad(na, dlo, v);
+            if (push_hi0) stc2ad(na, dhi, v);
+            if (push_hi1) stc2ad(na, nx8 + dhi, u);
+          }
         }
         if (TM) tmem_st8(tbase + cc * 16 + 8 * (1 - PAR), v, u);   // Y_{s+1} replaces Y_{s-1}
       }
@@ -1009,11 +1053,31 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
   // after my wait (acquire); a push of step s + 1 into buffer ca(s) happens after the pusher's wait of
   // step s, i.e. after every thread of this CTA finished reading ca(s) in step s.
   const bool edge_w = __any_sync(0xffffffffu, (lr0 == 0) || (lr0 + 2 >= rows));
+  // split == 2 (neighbour sync): no cluster barrier in the loop.  The ghost rows a step reads were pushed
+  // by the neighbours' previous step with st.async, which completes transaction bytes on this CTA's
+  // mbarrier of that buffer; thread 0 arms it (arrive.expect_tx with the bytes the neighbours will push)
+  // one step ahead, the edge warps wait on it, the CTA synchronises once per step.  A neighbour pushes
+  // into buffer p again (two steps later) only after it received this CTA's pushes of the step between,
+  // which each pushing thread issues after reading its ghost values: no ghost row is overwritten early.
+  // (the CTA below pushes only if this slab has rows: an empty top CTA of the cluster receives nothing)
+  const unsigned row_bytes = 8u * (unsigned)nx * (unsigned)((has_lo && rows > 0 ? 1 : 0) + (has_hi ? 1 : 0));
   auto pre = [&](int st) {
+    if (split == 2) {
+      if (tid == 0) {                                      // arm gmb[na parity] for this step's pushes
+        unsigned cols = 0;
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) cols += (st + 1 < mcol[cc]) ? 1u : 0u;
+        mb_arrive_tx(gmb32 + 8u * (unsigned)((st + 1) & 1), cols * row_bytes);
+      }
+      if (st > 0 && edge_w) mb_wait_cluster(gmb32 + 8u * (unsigned)(st & 1), (unsigned)((st - 1) >> 1) & 1u);
+      return;
+    }
     if (split && st > 0 && edge_w) cluster_wait();
   };
   auto post = [&](int st) {
-    if (split) {
+    if (split == 2) {
+      __syncthreads();
+    } else if (split) {
       if (st > 0 && !edge_w) cluster_wait();
       cluster_arrive();
       __syncthreads();
@@ -1031,7 +1095,8 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
       post(st + 1);
     }
   }
-  if (split && mrun > 0) cluster_wait();                   // the last arrive: no CTA leaves while pushed to
+  if (split == 2) cluster_barrier();                       // nothing in flight; no CTA leaves early
+  else if (split && mrun > 0) cluster_wait();              // the last arrive: no CTA leaves while pushed to
   if (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -1639,13 +1704,14 @@ static bool filter_tmem(unsigned threads) {
   const char* e = getenv("SCSF_FILTER_TMEM");
   return !(e && e[0] == '0');
 }
-// The split arrive / wait step synchronisation of k_filter_cl is the default; SCSF_FILTER_SPLIT = 0
-// restores one cluster barrier per step (read per call).  Measured (tools/bench_filter.py, m = 160,
-// profiles/r02_filter_split_ab.json): C3 filter 3.611 -> 3.489 ms, C2 0.440 -> 0.431 ms; C3 bench
-// 45.5 -> 46.5 operators/s.
+// Step synchronisation of k_filter_cl (SCSF_FILTER_SPLIT, read per call): 2 (default) = mbarrier
+// neighbour sync with st.async ghost pushes, 1 = split cluster arrive / wait, 0 = one cluster barrier per
+// step.  Measured (tools/bench_filter.py, m = 160, profiles/r02_filter_split_ab.json): C3 filter
+// 3.611 (0) -> 3.489 (1) ms, and in another run 3.634 (1) -> 3.332 (2) ms; C2 0.444 -> 0.424 ms;
+// C3 bench 45.6 (1) -> 48.2 (2) operators/s.
 static int filter_split() {
   const char* e = getenv("SCSF_FILTER_SPLIT");
-  return (e && e[0] == '0') ? 0 : 1;
+  return (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
 }
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,

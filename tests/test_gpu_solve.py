@@ -93,7 +93,7 @@ def test_filter_matches_oracle(lib, cfg_name, nx, k, m, streaming, monkeypatch):
 
 @pytest.mark.parametrize("cfg_name,nx,k,m", [("C3", 200, 5, 20), ("C3", 190, 3, 9), ("C2", 100, 6, 20),
                                              ("C2", 92, 5, 21), ("C3", 76, 4, 9), ("C1", 132, 3, 20)])
-@pytest.mark.parametrize("split,tmem", [("0", "1"), ("1", "1"), ("1", "0")])
+@pytest.mark.parametrize("split,tmem", [("0", "1"), ("1", "1"), ("1", "0"), ("2", "1"), ("2", "0")])
 def test_filter_tmem_variant(lib, cfg_name, nx, k, m, split, tmem, monkeypatch):
     """k_filter_cl with the patch rows of Y_s / Y_{s-1} in tensor memory (SCSF_FILTER_TMEM=1: tcgen05
     alloc / st / ld / dealloc) against the oracle, on 16-CTA (nx 190/200) and 8-CTA clusters with ragged
@@ -377,9 +377,10 @@ def test_adaptive_degree_matches_oracle(lib, cfg_name, nx, L, n_ops, cap):
 
 @pytest.mark.parametrize("degree", [40, -40])
 def test_filter_split_sync_bitwise(lib, degree, monkeypatch):
-    """The split arrive / wait step synchronisation of k_filter_cl changes no arithmetic: a C3-shaped
-    chain (200 x 200, the 16-CTA cluster kernel) solved with SCSF_FILTER_SPLIT=1 returns bitwise the
-    eigenpairs of the default per-step cluster barrier, uniform and per-column degrees."""
+    """The step synchronisation of k_filter_cl changes no arithmetic: a C3-shaped chain (200 x 200, the
+    16-CTA cluster kernel, an empty top CTA) solved with the split arrive / wait (SCSF_FILTER_SPLIT=1) or
+    the mbarrier neighbour sync with st.async ghost pushes (=2) returns bitwise the eigenpairs of the
+    per-step cluster barrier (=0), uniform and per-column degrees."""
     import torch
     monkeypatch.delenv("SCSF_FILTER_STREAMING", raising=False)
     cfg = synth.get_config("C3").with_(L=24)
@@ -387,9 +388,10 @@ def test_filter_split_sync_bitwise(lib, degree, monkeypatch):
     ops, params = device_problem(f)
     perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
     out = []
-    for split in ("0", "1"):
+    for split in ("0", "1", "2"):
         monkeypatch.setenv("SCSF_FILTER_SPLIT", split)
         ev, vec, st = lib.solve_queue(ops, perm, cfg.L, cfg.nex, degree, cfg.tol, 400, seed=9)
         assert all(s["status"] == 0 for s in st), st
         out.append((ev.cpu(), vec.cpu()))
-    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    for k in (1, 2):
+        assert torch.equal(out[0][0], out[k][0]) and torch.equal(out[0][1], out[k][1]), k
