@@ -51,8 +51,10 @@ CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 # unconverged (CholQR breakdown, profiles/r02_degree_limit_C3.jsonl), m = 160 / 192 none; since the
 # device-side conditioning cap (reading R28) and the cold retry every m converges, and with the
 # neighbour-sync filter m = 160 / 192 / 224 / 256 give 46.6 / 47.2 / 47.4 / 47.3 operators/s
-# (profiles/r02_degree_sweep_s2.json): C3 runs at 192, just above where the cap starts to bind.
-BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": 192, "C4": 80, "C5": 80}
+# (profiles/r02_degree_sweep_s2.json).  C3 runs with Alg. 1's per-column degrees (degree < 0, P:175,
+# SURVEY f2; the library's k_lock sets each column's m_j <= |degree|): at this degree they pay,
+# 52.3 / 53.6 operators/s at max 192 / 256 against 49.1 uniform at 192 (profiles/r02_f2_sweep_C3.json).
+BENCH_DEGREE = {"C1": 20, "C2": 20, "C3": -256, "C4": 80, "C5": 80}
 DEFAULT_CONFIG = "C3"
 
 
@@ -104,6 +106,8 @@ def workload_desc(cfg, n_total, world, degree):
         "grid": [cfg.nx] * cfg.dim, "n": cfg.n, "N_total": n_total, "N_per_gpu": n_total // world,
         "L": cfg.L, "nex": cfg.nex, "block": cfg.b, "degree": degree, "paper_degree": cfg.degree, "tol": cfg.tol,
         "p0": cfg.p0, "max_iter": cfg.max_iter,
+        # degree < 0: Alg. 1's per-column degrees, each column's m_j <= |degree|
+        "filter_degree": ({"per_column": True, "max": -degree} if degree < 0 else {"per_column": False, "m": degree}),
     }
 
 
