@@ -293,23 +293,31 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-__global__ void __launch_bounds__(TNT_NT) k_gemm_tn_tma(const __grid_constant__ CUtensorMap tmX,
+// TW = 64: 4 consumer warps of 32 x 32 (2 CTAs per SM); TW = 128 (b1 > 128): 8 consumer warps of
+// 32 x 64 on a 128 x 128 tile, twice the flops per operand byte of the 64-wide tile (one CTA per SM,
+// 6 stages of 2 x 16 KB).  Boxes are 16 rows x TW columns; the swizzled fragment addressing is the
+// same (a box column is one 128-byte row).
+template <int TW>
+__global__ void __launch_bounds__(32 * (TW / 16 + 1)) k_gemm_tn_tma(const __grid_constant__ CUtensorMap tmX,
                                                       const __grid_constant__ CUtensorMap tmY,
                                                       const __grid_constant__ CUtensorMap tmY2, int dual, int b1,
                                                       int b2, int64_t n, int64_t kchunk, int upper,
                                                       double* __restrict__ P) {
+  constexpr int NCW = TW / 16;                       // consumer warps: (TW / 32) rows x 2 columns of warps
+  constexpr int NI = TW / 16;                        // 8-column DMMA blocks per warp (warp tile 32 x TW / 2)
+  constexpr int TILE_BYTES = TW * TNT_BOX_R * 8;
   extern __shared__ __align__(1024) unsigned char tsm[];
   // 1024-byte aligned ring: [TNT_ST] x {X box, Y box}; then the barriers
   unsigned char* base = tsm + ((1024 - (smem_u32(tsm) & 1023)) & 1023);
   const uint32_t ring = smem_u32(base);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TNT_ST * 2 * TNT_TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TNT_ST * 2 * TILE_BYTES);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * TNT_ST;
 
-  const int T2 = (b2 + V2_T - 1) / V2_T;
+  const int T2 = (b2 + TW - 1) / TW;
   const int grp = dual ? (int)blockIdx.y / T2 : 0;
   const int ti = blockIdx.x, tj = dual ? (int)blockIdx.y % T2 : (int)blockIdx.y;
   if (upper && ti > tj) return;
-  const int i0 = ti * V2_T, j0 = tj * V2_T;
+  const int i0 = ti * TW, j0 = tj * TW;
   const int b2tot = dual ? 2 * b2 : b2;
   const int jout = grp * b2;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
@@ -320,64 +328,69 @@ __global__ void __launch_bounds__(TNT_NT) k_gemm_tn_tma(const __grid_constant__ 
   if (tid == 0) {
     for (int st = 0; st < TNT_ST; ++st) {
       mbar_init(full0 + 8 * st, 1);
-      mbar_init(empty0 + 8 * st, 4);
+      mbar_init(empty0 + 8 * st, NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == 4) {                                   // producer
+  if (warp == NCW) {                                 // producer
     if (lane == 0) {
       const CUtensorMap* my = grp ? &tmY2 : &tmY;
       for (int c = 0; c < nck; ++c) {
         const int st = c % TNT_ST;
         if (c >= TNT_ST) mbar_wait(empty0 + 8 * st, ((c / TNT_ST) - 1) & 1);
         const uint32_t fb = full0 + 8 * st;
-        mbar_expect_tx(fb, 2 * TNT_TILE_BYTES);
+        mbar_expect_tx(fb, 2 * TILE_BYTES);
         const int k0 = (int)(kbeg + (int64_t)c * TNT_BOX_R);
-        tma_load_2d(ring + st * 2 * TNT_TILE_BYTES, &tmX, k0, i0, fb);
-        tma_load_2d(ring + st * 2 * TNT_TILE_BYTES + TNT_TILE_BYTES, my, k0, j0, fb);
+        tma_load_2d(ring + st * 2 * TILE_BYTES, &tmX, k0, i0, fb);
+        tma_load_2d(ring + st * 2 * TILE_BYTES + TILE_BYTES, my, k0, j0, fb);
       }
     }
     return;
   }
 
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const bool idle = (i0 + wm >= b1) || (j0 + wn >= b2) || (upper && ti == tj && wm > wn);
-  double acc[4][4][2];
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * (TW / 2);
+  // idle: past the operand, or (upper mode, diagonal tile) entirely below the diagonal
+  const bool idle = (i0 + wm >= b1) || (j0 + wn >= b2) || (upper && ti == tj && wm >= wn + TW / 2);
+  double acc[4][NI][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int c = 0; c < nck; ++c) {
     const int st = c % TNT_ST;
     mbar_wait(full0 + 8 * st, (c / TNT_ST) & 1);
     if (!idle) {
-      const unsigned char* xs = base + st * 2 * TNT_TILE_BYTES;
-      const unsigned char* ys = xs + TNT_TILE_BYTES;
+      const unsigned char* xs = base + st * 2 * TILE_BYTES;
+      const unsigned char* ys = xs + TILE_BYTES;
 #pragma unroll
       for (int kk = 0; kk < TNT_BOX_R; kk += 8) {
         const int u = (kk >> 1) + t;               // 16-byte unit: rows kk + 2t, kk + 2t + 1
-        double2 a[4], b[4];
+        double2 a[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int col = wm + 4 * g + mi;
           a[mi] = *reinterpret_cast<const double2*>(xs + col * 128 + ((u ^ (col & 7)) << 4));
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int col = wn + 4 * g + ni;
-          b[ni] = *reinterpret_cast<const double2*>(ys + col * 128 + ((u ^ (col & 7)) << 4));
+        for (int h = 0; h < NI / 4; ++h) {               // 32-column halves, each as in the 64-wide tile
+          double2 b[4];                                  // (one half's B fragments live at a time)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int col = wn + h * 32 + 4 * g + q;
+            b[q] = *reinterpret_cast<const double2*>(ys + col * 128 + ((u ^ (col & 7)) << 4));
+          }
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma(acc[mi][4 * h + q][0], acc[mi][4 * h + q][1], a[mi].x, b[q].x);
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma(acc[mi][4 * h + q][0], acc[mi][4 * h + q][1], a[mi].y, b[q].y);
         }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
       }
     }
     __syncwarp();
@@ -387,14 +400,30 @@ __global__ void __launch_bounds__(TNT_NT) k_gemm_tn_tma(const __grid_constant__ 
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int i = i0 + wm + 4 * g + mi, j = j0 + wn + 4 * (2 * t + e) + ni;
+        const int i = i0 + wm + 4 * g + mi, j = j0 + wn + (ni >> 2) * 32 + 4 * (2 * t + e) + (ni & 3);
         if (i < b1 && j < b2) out[i + (int64_t)(j + jout) * b1] = acc[mi][ni][e];
       }
 }
-static size_t tnt_smem() { return (size_t)TNT_ST * 2 * TNT_TILE_BYTES + 2 * 8 * TNT_ST + 1024; }
+static size_t tnt_smem(int tw = V2_T) { return (size_t)TNT_ST * 2 * tw * TNT_BOX_R * 8 + 2 * 8 * TNT_ST + 1024; }
+// SCSF_TN_WIDE=1: 128-wide TMA tiles for b1, b2 > 128 (off by default).  Measured (tools/gemm_ab.py,
+// profiles/r02_tn_wide_ab.json): the full C3-shape TN 276.8 -> 209.3 us (16.6 -> 22.0 TF/s), C5 upper
+// Gram 2377 -> 1795 us, but C5 full 3974 -> 4127 us, and in the solver the C3 bench went 53.6 -> 52.7
+// operators/s: locking shrinks the active block below 129 columns within an iteration or two, so few
+// calls qualify, and the one-CTA-per-SM 192 KB tiles crowd the concurrent chains' filter clusters.
+static bool tn_wide_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCSF_TN_WIDE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+// splits of a 128-wide TN product: about one wave of one CTA per SM, within the partial-sum workspace
+// (tn_partial_doubles: at least 4 148 64^2 + 2 b1 b2 doubles for this call's b1, b2)
+static int tn_wide_splits(int64_t n, int b1, int b2tot, int tiles, int64_t cap_doubles);
 
 // Tensor map of a column-major n x cols operand (ld doubles): dim 0 = rows (contiguous), dim 1 =
 // columns, box 16 rows x 64 columns, 128-byte swizzle; out-of-range rows / columns read as zero.
@@ -891,7 +920,9 @@ int dense_init_attrs() {
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        NN_MAX_K * NN_LDS * (int)sizeof(double)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn2_smem()));
-  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tnt_smem()));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tnt_smem(64)));
+  SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn_tma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tnt_smem(128)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn2_smem(NN2_MAX_K)));
   SCSF_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_nn3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -918,6 +949,13 @@ static int tn_min_rows() {
     if (v < 32) v = 32;
   }
   return v;
+}
+
+static int tn_wide_splits(int64_t n, int b1, int b2tot, int tiles, int64_t cap_doubles) {
+  const int want = max(1, (148 + tiles - 1) / tiles);
+  const int maxs = max(1, (int)ceil_div(n, (int64_t)tn_min_rows()));
+  const int cap = max(1, (int)(cap_doubles / ((int64_t)b1 * b2tot)));
+  return min(min(want, maxs), cap);
 }
 
 int tn_splits(int64_t n, int b1, int b2) {
@@ -953,10 +991,23 @@ int gemm_tn(const double* X, int64_t ldx, int b1, const double* Y, int64_t ldy, 
   splits = ceil_div(n, kchunk);
   dim3 g(ceil_div(b1, V2_T), ceil_div(b2, V2_T), splits);
   if (tma_ok(X, ldx, n) && tma_ok(Y, ldy, n) && tma_encode_fn() == SCSF_OK) {
-    CUtensorMap mx, my;
-    SCSF_TRY(make_tmap(&mx, X, ldx, n, b1));
-    SCSF_TRY(make_tmap(&my, Y, ldy, n, b2));
-    k_gemm_tn_tma<<<g, TNT_NT, tnt_smem(), s>>>(mx, my, my, 0, b1, b2, n, kchunk, upper, P);
+    if (b1 > 128 && b2 > 128 && tn_wide_enabled()) {           // 128 x 128 tiles, 8 consumer warps
+      const int t1 = ceil_div(b1, 128), t2 = ceil_div(b2, 128);
+      const int tiles = upper ? t1 * (t1 + 1) / 2 : t1 * t2;
+      splits = tn_wide_splits(n, b1, b2, tiles, (int64_t)4 * 148 * TN_BM * TN_BM + (int64_t)2 * b1 * b2);
+      kchunk = round_up(ceil_div(n, splits), TN_KC);
+      splits = (int)ceil_div(n, kchunk);
+      CUtensorMap mx, my;
+      SCSF_TRY(make_tmap(&mx, X, ldx, n, b1, TNT_BOX_R, 128));
+      SCSF_TRY(make_tmap(&my, Y, ldy, n, b2, TNT_BOX_R, 128));
+      k_gemm_tn_tma<128><<<dim3(t1, t2, splits), 32 * 9, tnt_smem(128), s>>>(mx, my, my, 0, b1, b2, n, kchunk, upper,
+                                                                           P);
+    } else {
+      CUtensorMap mx, my;
+      SCSF_TRY(make_tmap(&mx, X, ldx, n, b1));
+      SCSF_TRY(make_tmap(&my, Y, ldy, n, b2));
+      k_gemm_tn_tma<64><<<g, TNT_NT, tnt_smem(64), s>>>(mx, my, my, 0, b1, b2, n, kchunk, upper, P);
+    }
   } else {
     const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y & 15) == 0) ? 1 : 0;
     k_gemm_tn2<<<g, V2_NT, tn2_smem(), s>>>(X, ldx, b1, Y, ldy, b2, n, kchunk, upper, a16, P, nullptr);
@@ -982,11 +1033,24 @@ int gemm_tn_dual(const double* X, int64_t ldx, const double* Y1, const double* Y
   splits = ceil_div(n, kchunk);
   dim3 g(t, 2 * t, splits);
   if (tma_ok(X, ldx, n) && tma_ok(Y1, ldy, n) && tma_ok(Y2, ldy, n) && tma_encode_fn() == SCSF_OK) {
-    CUtensorMap mx, m1, m2;
-    SCSF_TRY(make_tmap(&mx, X, ldx, n, b));
-    SCSF_TRY(make_tmap(&m1, Y1, ldy, n, b));
-    SCSF_TRY(make_tmap(&m2, Y2, ldy, n, b));
-    k_gemm_tn_tma<<<g, TNT_NT, tnt_smem(), s>>>(mx, m1, m2, 1, b, b, n, kchunk, 1, P);
+    if (b > 128 && tn_wide_enabled()) {                        // 128 x 128 tiles, 8 consumer warps
+      const int tw = ceil_div(b, 128);
+      splits = tn_wide_splits(n, b, 2 * b, tw * (tw + 1), (int64_t)4 * 148 * TN_BM * TN_BM + (int64_t)2 * b * b);
+      kchunk = round_up(ceil_div(n, splits), TN_KC);
+      splits = (int)ceil_div(n, kchunk);
+      CUtensorMap mx, m1, m2;
+      SCSF_TRY(make_tmap(&mx, X, ldx, n, b, TNT_BOX_R, 128));
+      SCSF_TRY(make_tmap(&m1, Y1, ldy, n, b, TNT_BOX_R, 128));
+      SCSF_TRY(make_tmap(&m2, Y2, ldy, n, b, TNT_BOX_R, 128));
+      k_gemm_tn_tma<128><<<dim3(tw, 2 * tw, splits), 32 * 9, tnt_smem(128), s>>>(mx, m1, m2, 1, b, b, n, kchunk, 1,
+                                                                                P);
+    } else {
+      CUtensorMap mx, m1, m2;
+      SCSF_TRY(make_tmap(&mx, X, ldx, n, b));
+      SCSF_TRY(make_tmap(&m1, Y1, ldy, n, b));
+      SCSF_TRY(make_tmap(&m2, Y2, ldy, n, b));
+      k_gemm_tn_tma<64><<<g, TNT_NT, tnt_smem(64), s>>>(mx, m1, m2, 1, b, b, n, kchunk, 1, P);
+    }
   } else {
     const int a16 = (((ldx | ldy) & 1) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Y1 & 15) == 0 &&
                      ((uintptr_t)Y2 & 15) == 0) ? 1 : 0;
