@@ -40,7 +40,10 @@ def _stencil_apply(coef, nx, ny, V):
     return Y
 
 
-def test_c2_full_queue_32_chains(lib):
+@pytest.mark.parametrize("degree", [None, -80])
+def test_c2_full_queue_32_chains(lib, degree):
+    """configs[1] at full N in 32 chains, at the paper's m = 20 and at bench.py's launch configuration
+    (per-column degrees up to 80): every pair's residual and orthogonality, oracle on a sample."""
     import torch
     cfg = synth.get_config("C2")
     f = synth.make_batch(cfg)
@@ -48,7 +51,8 @@ def test_c2_full_queue_32_chains(lib):
     ops, params = device_problem(f)
     perm, _, _ = lib.sort(params, cfg.dim, cfg.nx, cfg.p0)
     n_chains = 32
-    evals, evecs, stats = lib.solve_chains(ops, perm, n_chains, cfg.L, cfg.nex, cfg.degree, cfg.tol, cfg.max_iter,
+    m = cfg.degree if degree is None else degree
+    evals, evecs, stats = lib.solve_chains(ops, perm, n_chains, cfg.L, cfg.nex, m, cfg.tol, cfg.max_iter,
                                            seed=12345)
     torch.cuda.synchronize()
     assert all(s["status"] == 0 for s in stats), [i for i, s in enumerate(stats) if s["status"] != 0]
@@ -85,7 +89,8 @@ def test_c2_full_queue_32_chains(lib):
     assert np.all(lo <= ev[0] * (1 + 1e-12)) and np.all(ev[0] <= hi * (1 + 1e-12))
 
 
-@pytest.mark.parametrize("name,degree", [("C3", None), ("C4", None), ("C3", 192), ("C3", 256), ("C3", -256)])
+@pytest.mark.parametrize("name,degree", [("C3", None), ("C4", None), ("C3", 192), ("C3", 256), ("C3", -256),
+                                         ("C4", -256)])
 def test_full_queue_properties(lib, name, degree):
     """configs[2] / configs[3] at full N through scsf_solve_chains (32 chains), as bench.py runs
     them.  Every operator converges to the paper metric, its Ritz values ascend and sit
@@ -95,8 +100,8 @@ def test_full_queue_properties(lib, name, degree):
     Sylvester inertia counts show that no eigenvalue below lam_L was missed.
     degree = 256 on C3 is past CholQR's stability ceiling (R27: 130 of 400 operators
     failed before the guard); the device-side degree cap (R28) must lower it where needed so
-    that every operator still converges to the same pairs.  degree = -256 is bench.py's C3 launch
-    configuration (BENCH_DEGREE, 32 chains): Alg. 1's per-column degrees up to 256."""
+    that every operator still converges to the same pairs.  degree = -256 is bench.py's C3 and C4
+    launch configuration (BENCH_DEGREE, 32 chains): Alg. 1's per-column degrees up to 256."""
     import os
     import torch
     cfg = synth.get_config(name)
