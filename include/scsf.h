@@ -222,8 +222,8 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  * ChFSI for one operator, Alg. 3: the L smallest eigenpairs of
  * A^(op_index) to relative residual ||Av - lv||/||Av|| <= tol.
  *  nex       extra (inherited) subspace columns: block b = L + nex (R12)
- *  degree    Chebyshev filter degree m (default 20).  m in [1, 384]: every active
- *            column is filtered with degree m (reading R8).  m in [-384, -4]: per-column
+ *  degree    Chebyshev filter degree m (default 20).  m in [1, 256]: every active
+ *            column is filtered with degree m (reading R8).  m in [-256, -4]: per-column
  *            degrees (Alg. 1 l. 5's staggered update, the ChASE-style
  *            variant the paper cites): after each Rayleigh-Ritz step column j gets
  *            the degree its residual and Ritz value need to reach 0.1 tol, clamped to
@@ -245,8 +245,8 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  *            entry positive, R21); may alias warm_vecs.
  *  ld_vec    leading dimension of warm_vecs / evecs (>= n).
  *  st        host out (may be NULL).
- * Errors: SCSF_ERR_ARG (L < 1, nex < 0, L + nex > n, degree outside [1, 384] and
- * [-384, -4], tol <= 0),
+ * Errors: SCSF_ERR_ARG (L < 1, nex < 0, L + nex > n, degree outside [1, 256] and
+ * [-256, -4], tol <= 0),
  * SCSF_ERR_WORKSPACE, SCSF_ERR_NUMERICAL (not converged; outputs hold the
  * best pairs found and st->max_rel_resid the worst residual).
  */

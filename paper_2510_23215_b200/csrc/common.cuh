@@ -10,7 +10,7 @@
 namespace scsf {
 
 // filter parameter block: {lambda, c, e, -} then the per-step (a_s, b_s) table (k_step_table)
-constexpr int FP_TAB = 4, FP_MAX_DEGREE = 384, FP_DOUBLES = FP_TAB + 2 * FP_MAX_DEGREE;
+constexpr int FP_TAB = 4, FP_MAX_DEGREE = 256, FP_DOUBLES = FP_TAB + 2 * FP_MAX_DEGREE;
 // fp[3]: degree cap of the solver's next filter (k_lock / k_bounds_from_theta, conditioning guard);
 // 0 = none (the standalone scsf_cheb_filter).  Every filter kernel runs min(m, cap) steps.
 __device__ __forceinline__ int fp_degree_cap(const double* fp, int m) {

@@ -275,7 +275,7 @@ def test_bad_arguments(lib):
     f = synth.make_batch(synth.get_config("C1").with_(nx=6), 1)
     ops, _ = device_problem(f)
     for L, nex, m, tol in [(0, 1, 20, 1e-8), (30, 10, 20, 1e-8), (4, 1, 0, 1e-8), (4, 1, 20, 0.0), (4, 1, -3, 1e-8),
-                           (4, 1, 385, 1e-8), (4, 1, -385, 1e-8)]:
+                           (4, 1, 257, 1e-8), (4, 1, -257, 1e-8)]:
         with pytest.raises(lib.ScsfError) as ei:
             lib.solve_one(ops, 0, L, nex, m, tol, 10)
         assert ei.value.code == lib.SCSF_ERR_ARG
