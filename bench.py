@@ -56,7 +56,8 @@ CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 # 52.3 / 53.6 operators/s at max 192 / 256 against 49.1 uniform at 192 (profiles/r02_f2_sweep_C3.json).
 # C2 / C4 likewise (profiles/r02_f2_sweep_C2_C4.json): C2 1532 (m = 20) -> 2760 (per column <= 80),
 # C4 30.5 (m = 80) -> 33.6 (per column <= 256) operators/s.
-# C5 (row partition, one chain): 4.99 / 5.64 / 6.27 operators/s at m = 80 / per column <= 120 / <= 160.
+# C5 (row partition, one chain; the slab step honours per-column degrees since session 2): 4.99 at
+# m = 80, 6.57 / 6.80 / 6.06 operators/s at per column <= 120 / 160 / 256.
 BENCH_DEGREE = {"C1": 20, "C2": -80, "C3": -256, "C4": -256, "C5": -160}
 DEFAULT_CONFIG = "C3"
 

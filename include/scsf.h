@@ -228,9 +228,10 @@ size_t scsf_solve_workspace_bytes(const scsf_ops* ops, int32_t L, int32_t nex);
  *            variant the paper cites): after each Rayleigh-Ritz step column j gets
  *            the degree its residual and Ritz value need to reach 0.1 tol, clamped to
  *            [4, |m|]; finished columns are left untouched by the remaining steps.
- *            Honoured by the resident filters and the vectorised streaming step
- *            (5-/7-point operators, nx % 4 == 0); elsewhere (13-point family, row
- *            partition) it falls back to the uniform degree |m|.
+ *            Honoured by the resident filters, the vectorised streaming step
+ *            (5-/7-point operators, nx % 4 == 0) and the row partition's slab step
+ *            (scsf_solve_queue_dist); elsewhere (13-point family, scalar streaming
+ *            step) it falls back to the uniform degree |m|.
  *            Conditioning guard (R28): each filter runs at most the degree
  *            for which C_m(t_lambda) = cosh(m acosh|(lambda - c)/e|) <= 1e8 (rounded
  *            down to = m mod 3, >= 4), so a degree past CholQR's stability ceiling

@@ -1427,15 +1427,19 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
     const double* __restrict__ cf, int64_t ldc, int nx, int64_t n_glob, int64_t goff, int64_t n_loc,
     const double* __restrict__ X, const double* Xp, double* Out, int64_t ldv, int ncols,
     const double* __restrict__ ghost_lo, const double* __restrict__ ghost_hi, const double* __restrict__ fp,
-    int step, int64_t l_begin, int64_t l_end) {
+    int step, int64_t l_begin, int64_t l_end, const int* __restrict__ deg) {
   const int64_t l0 = l_begin + ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;   // local point
   if (l0 >= l_end) return;
   double a, b, c;
   if (!step_scalars(fp, step, a, b, c)) return;
   const int j0 = blockIdx.y * CB;
   const int j1 = min(ncols, j0 + CB);
+  // per-column degrees (deg != NULL only for filter steps): a column past its degree is
+  // left untouched (its last output already sits in the buffer of Y_m, k_lock's mod-3 rounding)
+  auto live = [&](int j) { return j < j1 && (deg == nullptr || step < __ldg(deg + j)); };
   if (l0 >= n_loc) {                                  // ld padding
-    for (int j = j0; j < j1; ++j) stg4(Out + (int64_t)j * ldv + l0, make_double4(0, 0, 0, 0));
+    for (int j = j0; j < j1; ++j)
+      if (live(j)) stg4(Out + (int64_t)j * ldv + l0, make_double4(0, 0, 0, 0));
     return;
   }
   const int64_t k0 = goff + l0;                       // global point
@@ -1458,7 +1462,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       const int j = j0 + g0 + q;
-      if (j < j1) {
+      if (live(j)) {
         const double* __restrict__ x = X + (int64_t)j * ldv;
         xc[q] = ldg4_nc(x + l0);
         xl[q] = hm ? __ldg(x + l0 - 1) : 0.0;
@@ -1473,7 +1477,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_slab(
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       const int j = j0 + g0 + q;
-      if (j < j1) {
+      if (live(j)) {
         double4 v;
         v.x = (dg.x - c) * xc[q].x + cxp.x * xc[q].y + cxm * xl[q] + cyp.x * xu[q].x + cym.x * xd[q].x;
         v.y = (dg.y - c) * xc[q].y + cxp.y * xc[q].z + cxp.x * xc[q].x + cyp.y * xu[q].y + cym.y * xd[q].y;
@@ -1502,7 +1506,8 @@ int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncol
 // together equal part 0, so the halo exchange can run while part 1 computes.
 int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
                       double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
-                      const double* fp, int step, cudaStream_t s, int part) {
+                      const double* fp, int step, cudaStream_t s, int part, const int* deg) {
+  if (step < 0) deg = nullptr;                         // A X passes use every column
   if (ncols <= 0) return SCSF_OK;
   const int64_t n_glob = (int64_t)ops->nx * ops->ny;
   const int nx = ops->nx;
@@ -1512,7 +1517,7 @@ int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, 
     if (le <= lb) return SCSF_OK;
     dim3 g(ceil_div(ceil_div(le - lb, 4), SV_THREADS), ceil_div(ncols, CB));
     k_stencil_slab<CB><<<g, SV_THREADS, 0, s>>>(cf, ops->ld, nx, n_glob, goff, n_loc, X, Xp, Out, ldv, ncols,
-                                                ghost_lo, ghost_hi, fp, step, lb, le);
+                                                ghost_lo, ghost_hi, fp, step, lb, le, deg);
     SCSF_LAUNCH_CHECK();
     return SCSF_OK;
   };

@@ -65,7 +65,7 @@ int pack_rows_impl(const double* X, int64_t ldv, int64_t n_loc, int nx, int ncol
                    double* send_hi, cudaStream_t s);
 int stencil_slab_impl(const scsf_ops* ops, int op, int64_t goff, int64_t n_loc, const double* X, const double* Xp,
                       double* Out, int64_t ldv, int ncols, const double* ghost_lo, const double* ghost_hi,
-                      const double* fp, int step, cudaStream_t s, int part = 0);
+                      const double* fp, int step, cudaStream_t s, int part = 0, const int* deg = nullptr);
 int colmax_local_impl(const double* V, int64_t ldv, int64_t n, const int* perm, int b, int64_t goff, double* colbuf,
                       cudaStream_t s);
 int sort_theta_impl(const double* theta, const double* rel, int b, int L, int* perm, double* theta_sorted,
@@ -248,11 +248,11 @@ static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const 
   const double* glo = w.comm->rank > 0 ? w.recv_lo : nullptr;
   const double* ghi = w.comm->rank + 1 < w.comm->world ? w.recv_hi : nullptr;
   if (w.comm->world == 1)                          // one slab: no neighbour, no exchange
-    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0);
+    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0, deg);
   SCSF_TRY(pack_rows_impl(X, w.ldv, w.n, w.nx, ncols, w.send_lo, w.send_hi, s));
   if (!halo_overlap()) {
     SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, s));
-    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0);
+    return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 0, deg);
   }
   HaloStreams* hs;
   SCSF_TRY(halo_streams(hs));
@@ -260,9 +260,9 @@ static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const 
   SCSF_CUDA_CHECK(cudaStreamWaitEvent(hs->side, hs->packed, 0));
   SCSF_TRY(w.comm->halo(w.send_lo, w.send_hi, w.recv_lo, w.recv_hi, (size_t)ncols * w.nx, hs->side));
   SCSF_CUDA_CHECK(cudaEventRecord(hs->landed, hs->side));
-  SCSF_TRY(stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 1));
+  SCSF_TRY(stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 1, deg));
   SCSF_CUDA_CHECK(cudaStreamWaitEvent(s, hs->landed, 0));
-  return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 2);
+  return stencil_slab_impl(ops, op, w.goff, w.n, X, Xp, Out, w.ldv, ncols, glo, ghi, w.fp, step, s, 2, deg);
 }
 
 // Q = CholQR pass on columns [0, ncols) of Y (in place, or into Out when Out != Y).
@@ -580,7 +580,10 @@ int solve_core(const scsf_ops* ops_in, int op_in, int L, int nex, int degree_arg
   SCSF_TRY(gershgorin_impl(ops, op, w.gersh, s));
   SCSF_TRY(ctrl_init_impl(w.ctrl, w.gersh, s));
   w.mdeg = degree;
-  w.deg_on = (adaptive && !w.comm && (filter_resident_ok(ops) || stencil_v4_ok(ops, w.ldv))) ? w.deg : nullptr;
+  // per-column degrees where the filter kernel honours them: the resident filters, the vectorised
+  // streaming step and (row partition, always nx % 4 == 0) the slab step; the degrees come from
+  // k_lock on all-reduced residuals, so every rank of a partition picks the same ones
+  w.deg_on = (adaptive && (w.comm || filter_resident_ok(ops) || stencil_v4_ok(ops, w.ldv))) ? w.deg : nullptr;
   if (w.deg_on) SCSF_TRY(fill_int_impl(w.deg, b, degree, s));
   if (!warm) SCSF_TRY(rand_block_impl(w.V, w.ldv, w.n, b, seed, w.goff, s));
   if (!warm || orthonormalize) {

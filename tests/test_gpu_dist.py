@@ -92,6 +92,31 @@ def test_loopback_row_partition_matches_oracle(lib, world, nx):
     assert np.abs(ev0 - e1).max() <= 1e-10 * np.abs(e1).max()
 
 
+@pytest.mark.parametrize("world,nx", [(1, 40), (2, 40), (3, 36)])
+def test_loopback_row_partition_adaptive_degree(lib, world, nx):
+    """Per-column degrees (degree < 0, Alg. 1 l. 5's staggered update P:175) through the
+    row partition's slab step: every rank picks the same degrees (k_lock on all-reduced residuals),
+    finished columns are skipped, and the pairs match the oracle and the one-GPU adaptive solve."""
+    cfg = synth.get_config("C5").with_(nx=nx, L=12)
+    f = synth.make_batch(cfg, 3)
+    ops, _ = device_problem(f)
+    chain = np.array([1, 2, 0], dtype=np.int32)
+    out = _run_loopback(lib, ops, chain, cfg.L, cfg.nex, world, degree=-40)
+    ev0 = out[0][0].cpu().numpy()
+    for r in range(1, world):
+        assert np.array_equal(out[r][0].cpu().numpy(), ev0)
+    V = _assemble_slabs(out, nx, f.n)
+    for k, i in enumerate(chain):
+        assert out[0][2][k]["status"] == 0, out[0][2][k]
+        check_pairs(f, int(i), ev0[k], V[k].T, cfg.L, paper_tol=PAPER_TOL_SLACK * cfg.tol)
+    ev1, _, st1 = lib.solve_queue(ops, chain, cfg.L, cfg.nex, -40, cfg.tol, cfg.max_iter, seed=11)
+    e1 = ev1.cpu().numpy()
+    assert np.abs(ev0 - e1).max() <= 1e-10 * np.abs(e1).max()
+    # fewer filtered column-steps than the uniform degree 40 would apply
+    it = sum(s["iterations"] for s in out[0][2])
+    assert sum(s["spmm_columns"] for s in out[0][2]) < it * (40 + 2) * (cfg.L + cfg.nex)
+
+
 def test_loopback_chain_head_random_block_is_partition_independent(lib):
     """The cold start draws the same global random block on any partition (global row hash):
     the 1-slab and 2-slab loopback solves of a chain head agree to rounding."""
