@@ -636,7 +636,8 @@ __device__ __forceinline__ int filter_degree_cap(double lam, double c, double e,
 constexpr double LOCK_FLOOR = 2.0;
 __global__ void k_lock(const double* __restrict__ theta, const double* __restrict__ res,
                        const double* __restrict__ wn, double* __restrict__ rel, int b, int L,
-                       double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg, int cap_on) {
+                       double tol, Ctrl* ctrl, double* fp, int* __restrict__ deg, int mdeg, int cap_on,
+                       double margin) {
   const int lane = threadIdx.x;            // one warp
   const int kL = ctrl->kL;
   // Reading R26: the test ||r|| <= tol ||Av|| is capped at the fp64 floor of a computed
@@ -704,7 +705,7 @@ __global__ void k_lock(const double* __restrict__ theta, const double* __restric
         const double t = fabs((theta[j] - c) / e), r = rel[j];
         if (t > 1.0 && isfinite(r)) {
           const double g = t + sqrt((t - 1.0) * (t + 1.0));
-          const double need = log(fmax(10.0 * r / tol, 1.0)) / log(g);
+          const double need = log(fmax(margin * r / tol, 1.0)) / log(g);
           const int nd = (int)fmin((double)mcap, fmax(4.0, ceil(need)));
           // round up to nd = m (mod 3): the streaming filter rotates three buffers, so a column
           // that stops after nd steps then holds its Y_nd in the same buffer as Y_m
@@ -1074,9 +1075,21 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
   return SCSF_OK;
 }
 
+// Per-column degrees (f2) aim each column's residual at tol / margin after the next filter;
+// SCSF_DEG_MARGIN overrides the default 10 (read once per process, A/B runs).
+static double deg_margin() {
+  static double v = -1.0;
+  if (v < 0.0) {
+    const char* e = getenv("SCSF_DEG_MARGIN");
+    const double x = e ? atof(e) : 10.0;
+    v = (x >= 1.0) ? x : 10.0;
+  }
+  return v;
+}
+
 int lock_impl(const double* theta, const double* res, const double* wn, double* rel, int b, int L,
               double tol, Ctrl* ctrl, double* fp, int* deg, int mdeg, int cap_on, cudaStream_t s) {
-  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp, deg, mdeg, cap_on);
+  k_lock<<<1, 32, 0, s>>>(theta, res, wn, rel, b, L, tol, ctrl, fp, deg, mdeg, cap_on, deg_margin());
   SCSF_LAUNCH_CHECK();
   return SCSF_OK;
 }
