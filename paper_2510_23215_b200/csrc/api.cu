@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -29,11 +30,12 @@ void count_launch(int n) {
 }
 bool debug_sync() {
   if (t_capturing) return false;
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_DEBUG_SYNC");
     v = (e && e[0] == '1') ? 1 : 0;
-  }
+    return v;
+  }();
   return v == 1;
 }
 
@@ -61,6 +63,8 @@ int set_small_attrs();
 int dense_init_attrs();
 int stencil_init_attrs();
 static int init_kernel_attrs() {
+  static std::mutex mu;                    // API calls from several user threads: one initialiser at a time
+  std::lock_guard<std::mutex> lk(mu);
   SCSF_TRY(set_small_attrs());
   SCSF_TRY(dense_init_attrs());
   SCSF_TRY(stencil_init_attrs());

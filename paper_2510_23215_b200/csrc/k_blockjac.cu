@@ -224,12 +224,13 @@ __global__ void __launch_bounds__(512) k_bj_final(const double* __restrict__ Gp,
 // chains' graphs do not overlap as well); m = 120: unroll 4 / 5 / 6 / 8: 1.71 / 1.72 / 1.71 / 1.73 s,
 // and 6 sweeps never truncated a solve (3.58 sweeps per iteration, as the unbounded loop)
 static int bj_unroll() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_BJ_UNROLL");
     v = e ? atoi(e) : 6;
     if (v < 0) v = 0;
-  }
+    return v;
+  }();
   return v;
 }
 

@@ -414,11 +414,12 @@ static size_t tnt_smem(int tw = V2_T) { return (size_t)TNT_ST * 2 * tw * TNT_BOX
 // operators/s: locking shrinks the active block below 129 columns within an iteration or two, so few
 // calls qualify, and the one-CTA-per-SM 192 KB tiles crowd the concurrent chains' filter clusters.
 static bool tn_wide_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_TN_WIDE");
     v = (e && e[0] == '1') ? 1 : 0;
-  }
+    return v;
+  }();
   return v == 1;
 }
 // splits of a 128-wide TN product: about one wave of one CTA per SM, within the partial-sum workspace
@@ -462,20 +463,22 @@ static int make_tmap(CUtensorMap* m, const double* X, int64_t ld, int64_t n, int
 }
 // SCSF_TN_TMA=0 keeps the cp.async kernel (k_gemm_tn2) for A/B runs
 static bool tn_tma_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_TN_TMA");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 // SCSF_NN_TMA=0 keeps k_gemm_nn3 for the wide NN products (A/B runs)
 static bool nn_tma_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_NN_TMA");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 // TMA needs 16-byte aligned bases and leading dimensions (ld even) and row counts >= 16 to pay
@@ -886,28 +889,31 @@ static size_t nn3_smem(int b1, int pr) {
 // b = 240: 20.1 against 16.4 TF/s (k_gemm_nn2); b = 120 (C2): 10.0 against 10.8, and C2 runs
 // 5-9 % slower with it, so the 4-warp kernel keeps b <= 128.
 static int nn3_min_k() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_NN3_MIN_K");
     v = e ? atoi(e) : 128;
-  }
+    return v;
+  }();
   return v;
 }
 // k_gemm_nn_tma for inner dimensions above this (SCSF_NNT_MIN_K)
 static int nnt_min_k() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_NNT_MIN_K");
     v = e ? atoi(e) : 128;
-  }
+    return v;
+  }();
   return v;
 }
 static int nn3_big() {                             // SCSF_NN3_BIG=0: the v1 kernel for b1 > 256
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_NN3_BIG");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v;
 }
 static size_t nn2_smem(int b1) {
@@ -942,12 +948,13 @@ int dense_init_attrs() {
 // pipeline prologue and keep the partial-sum traffic small (with many concurrent chains the
 // GPU is full anyway, so per-CTA efficiency beats spreading one product over every SM).
 static int tn_min_rows() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_TN_MIN_ROWS");
     v = e ? atoi(e) : 512;
     if (v < 32) v = 32;
-  }
+    return v;
+  }();
   return v;
 }
 

@@ -1035,12 +1035,13 @@ static int jacobi_split_launch(const double* G, int64_t ldg, int b, double* scra
 // matrix (k_bj_offmax).  ctrl is not passed: hitting the inner cap is not a failure.  C3, one
 // chain: Rayleigh-Ritz 313 -> 272 ms per operator against solving every sub-problem to the end.
 static int bj_inner() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_BJ_INNER");
     v = e ? atoi(e) : 2;
     if (v < 1) v = 1;
-  }
+    return v;
+  }();
   return v;
 }
 int jacobi_batched_impl(const double* G, int64_t ldg, int bs, int batch, int64_t gstride, double* scratch,
@@ -1078,12 +1079,13 @@ int jacobi_impl(const double* G, int64_t ldg, int b, double* scratchG, double* Z
 // Per-column degrees (f2) aim each column's residual at tol / margin after the next filter;
 // SCSF_DEG_MARGIN overrides the default 10 (read once per process, A/B runs).
 static double deg_margin() {
-  static double v = -1.0;
-  if (v < 0.0) {
+  static const double v = [] {            // thread-safe one-time read (chain worker threads)
+    double v;
     const char* e = getenv("SCSF_DEG_MARGIN");
     const double x = e ? atof(e) : 10.0;
     v = (x >= 1.0) ? x : 10.0;
-  }
+    return v;
+  }();
   return v;
 }
 

@@ -1665,11 +1665,12 @@ static int cluster_size_for(const scsf_ops* ops) {
 
 // k_filter_rp: 2 x 4 register patches; SCSF_FILTER_RP=0 falls back to k_filter_cl
 static bool rp_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_FILTER_RP");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 static int rp_rows(int ny, int cs) { return ((ny + cs - 1) / cs + RP_ROWS - 1) / RP_ROWS * RP_ROWS; }

@@ -235,11 +235,12 @@ static int halo_streams(HaloStreams*& hs) {
   return SCSF_OK;
 }
 static bool halo_overlap() {                       // SCSF_HALO_OVERLAP=0: exchange, then one stencil launch
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_HALO_OVERLAP");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 static int spmm(const scsf_ops* ops, int op, SolveWS& w, const double* X, const double* Xp, double* Out, int ncols,
@@ -308,11 +309,12 @@ static int rayleigh_ritz(const scsf_ops* ops, int op, SolveWS& w, int k0, int L,
 // second triangular apply) and fuses two Gram passes into one.  The b x b
 // products are replicated (identical on every rank of a row partition).
 static bool fused_resid() {                         // SCSF_FUSED_RESID=0: W = A V then k_resid
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_FUSED_RESID");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 
@@ -358,21 +360,23 @@ static int rayleigh_ritz_q1(const scsf_ops* ops, int op, SolveWS& w, int k0, int
 // P:193-194 / P:297, reading R11); SCSF_INHERIT_BOUNDS=0 restores the extra Rayleigh-Ritz of
 // the new operator before the first filter.
 static bool inherit_bounds() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_INHERIT_BOUNDS");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1;
 }
 
 // SCSF_TRACE=1: one stderr line per outer iteration (diagnostics for tools/; host reads only)
 static bool trace_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_TRACE");
     v = (e && e[0] == '1') ? 1 : 0;
-  }
+    return v;
+  }();
   return v == 1;
 }
 
@@ -478,11 +482,12 @@ static std::unordered_map<GraphKey, std::shared_ptr<GraphExec>, GraphKeyHash>* g
 constexpr size_t GRAPH_CACHE_MAX = 20000;
 
 static bool graphs_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {            // thread-safe one-time read (chain worker threads)
+    int v;
     const char* e = getenv("SCSF_GRAPHS");
     v = (e && e[0] == '0') ? 0 : 1;
-  }
+    return v;
+  }();
   return v == 1 && !debug_sync();
 }
 
