@@ -1110,7 +1110,7 @@ __global__ void __launch_bounds__(CL_T, 1) k_filter_cl(const double* __restrict_
     double* out = Out + (int64_t)(j0 + cc) * ldv;
     for (int q = tid; q < rows * hx; q += nthr)
       *reinterpret_cast<double2*>(out + row0 * nx + 2 * q) = lds2(fin + nx + 2 * q);
-    if (rank == CS - 1)                                    // ld padding of the column
+    if (rank == (int)cluster.num_blocks() - 1)             // ld padding of the column (last CTA launched)
       for (int k = n + tid; k < (int)ldv; k += nthr) out[k] = 0.0;
   }
 }
@@ -1719,6 +1719,12 @@ static int filter_split() {
   const char* e = getenv("SCSF_FILTER_SPLIT");
   return (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
 }
+// SCSF_FILTER_TRIM (read per call): 1 (default) launches a cluster of only the CTAs whose slab holds
+// rows, 0 the template's full cluster size (the surplus CTAs idle through the filter).
+static bool filter_trim() {
+  const char* e = getenv("SCSF_FILTER_TRIM");
+  return !(e && e[0] == '0');
+}
 template <int CS, int CB>
 static cudaError_t launch_cl1(cudaLaunchConfig_t& cfg, const double* cf, int64_t ldc, int nx, int ny, const double* X,
                               int64_t ldv, int ncols, double* Out, const double* fp, int m, const int* deg) {
@@ -1835,14 +1841,17 @@ int filter_resident_impl(const scsf_ops* ops, int op, const double* X, double* O
     const size_t per_col = (size_t)2 * (R + 2) * ops->nx * sizeof(double);
     const int cb = (4 * per_col <= 200 * 1024) ? 4 : (2 * per_col <= 200 * 1024 ? 2 : 1);
     const int thr = (int)round_up((int64_t)(R / 2) * (ops->nx / 2), 32);
+    // launch only the CTAs whose slab holds rows: C3 (ny = 200, R = 14) needs 15 of the 16 the
+    // template's slab height is sized for, and an empty CTA would hold an SM for the whole filter
+    const int ccl = filter_trim() ? (int)ceil_div(ops->ny, R) : cs;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs, ceil_div(ncols, cb), 1);
+    cfg.gridDim = dim3(ccl, ceil_div(ncols, cb), 1);
     cfg.blockDim = dim3(thr, 1, 1);
     cfg.dynamicSmemBytes = per_col * cb;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.x = ccl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

@@ -395,3 +395,32 @@ def test_filter_split_sync_bitwise(lib, degree, monkeypatch):
         out.append((ev.cpu(), vec.cpu()))
     for k in (1, 2):
         assert torch.equal(out[0][0], out[k][0]) and torch.equal(out[0][1], out[k][1]), k
+
+
+@pytest.mark.parametrize("nx", [200, 198, 164, 92])
+def test_filter_trimmed_cluster_bitwise(lib, nx, monkeypatch):
+    """Launching only the CTAs whose slab holds rows (SCSF_FILTER_TRIM=1: 15 of 16 on 200 x 200 and
+    198 x 198, whose 14-row slabs cover 210 rows; 14 of 16 on 164 x 164; 92 x 92 fills its 8) changes
+    no arithmetic: the filtered block, including its zeroed ld padding (written by the last CTA
+    launched), is bitwise that of the full cluster, and both match the oracle (Alg. 1)."""
+    import torch
+    monkeypatch.delenv("SCSF_FILTER_STREAMING", raising=False)
+    cfg = synth.get_config("C3").with_(nx=nx)
+    f = synth.make_batch(cfg, 1)
+    ops, _ = device_problem(f)
+    n, ld, k, m = f.n, ops.ld, 7, 11
+    Y0 = np.random.default_rng(21).standard_normal((n, k))
+    A = oop.assemble_csr(f, 0)
+    normA = float(np.abs(A).sum(axis=1).max())
+    lam, alpha = 0.002 * normA, 0.1 * normA
+    c, e = (alpha + normA) / 2, (normA - alpha) / 2
+    outs = []
+    for trim in ("0", "1"):
+        monkeypatch.setenv("SCSF_FILTER_TRIM", trim)
+        Yd = torch.full((k, ld), 7.0, dtype=torch.float64, device="cuda")
+        Yd[:, :n] = torch.from_numpy(Y0.T.copy())
+        outs.append(lib.cheb_filter(ops, 0, Yd, m, lam, c, e).cpu())
+    assert torch.equal(outs[0], outs[1])
+    ref = ofilt.cheb_filter(A, Y0, m, lam, c, e)
+    Ym = _np_block(outs[1].cuda(), n)
+    assert np.all(np.abs(Ym - ref).max(axis=0) <= 1e-12 * np.abs(ref).max(axis=0))
