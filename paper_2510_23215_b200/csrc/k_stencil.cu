@@ -1647,6 +1647,13 @@ static bool cs16_ok() {
   return g_cs16.load(std::memory_order_acquire) == 1;
 }
 
+// SCSF_FILTER_CS_DOUBLE (read per call): 1 (default) doubles a cluster below 8 CTAs whose doubled slab
+// still has >= 8 rows (shorter filters); 0 keeps the smallest cluster that fits.  Co-resident clusters of
+// the filter's CTA shape on a B200 (tools/cluster_slots.cu): 33 of 4 CTAs (132 SMs), 15 of 8 (120 SMs).
+static bool filter_cs_double() {
+  const char* e = getenv("SCSF_FILTER_CS_DOUBLE");
+  return !(e && e[0] == '0');
+}
 static int cluster_size_for(const scsf_ops* ops) {
   if (ops->stencil != SCSF_STENCIL_FLUX || ops->dim != 2 || ops->nx % 2 != 0) return 0;
   // up to 16 CTAs (a non-portable cluster size, opted in per kernel): C3's 200 x 200 slabs fit at
@@ -1657,7 +1664,7 @@ static int cluster_size_for(const scsf_ops* ops) {
     const int R = ((ops->ny + cs - 1) / cs + 1) & ~1;
     if ((R / 2) * (ops->nx / 2) <= CL_MAXP && (size_t)2 * (R + 2) * ops->nx * sizeof(double) <= 200 * 1024) {
       const int R2 = ((ops->ny + 2 * cs - 1) / (2 * cs) + 1) & ~1;
-      return (cs < 8 && R2 >= 8) ? 2 * cs : cs;     // (the doubling stops at the portable 8)
+      return (cs < 8 && R2 >= 8 && filter_cs_double()) ? 2 * cs : cs;   // (the doubling stops at the portable 8)
     }
   }
   return 0;
